@@ -1,0 +1,21 @@
+"""B200-native hot path of the LPPLIC learned lossless codec (arXiv 2212.01185).
+
+Drop-in for the reference package's hot path
+(/root/reference/pkg/src/lpic/__init__.py:11-26): the same public names for
+the codec, network and schedule API.  Network evaluation, CDF construction,
+range coding and the wavefront decoder run in liblpic_b200.so (sm_100a) with
+no CPU fallback.  Training, CLI, image I/O and the scipy module ops of the
+reference are out of scope.
+"""
+
+from .codec import (CodecTrace, Container, bpsp, decode, decode_batch, encode, encode_batch,
+                    theoretical_bpsp)
+from .errors import CorruptStreamError, FingerprintMismatchError, LpicError, UnsupportedImageError
+from .network import (Distribution, ModelConfig, Weights, causal_taps, count_parameters, estimate_macs,
+                      forward_fc, forward_full, forward_patch, forward_taps_batch, glorot_weights,
+                      kaiming_weights, leaky_relu, load_weights, normalize, normalize_value, save_weights,
+                      weight_fingerprint, zero_weights)
+from .schedules import (Schedule, ScheduleMode, build_schedule, diagonal, parse_mode, sequential, validate,
+                        wavefront)
+
+__version__ = "0.1.0"

@@ -1,0 +1,703 @@
+// lpic_kernels.cu -- B200 (sm_100a) kernels and the C-ABI of liblpic_b200.so.
+//
+// Kernels (see DESIGN.md for rooflines):
+//   k_encode     fused encoder: causal gather -> network -> 3 quantised CDF
+//                tables per pixel -> packed (start,width) in coding order
+//                (codec.py:116-183, kernels.py:88-114, 296-313)
+//   k_rc_encode  one range-coder lane (warp) per stream (coder.py:30-73)
+//   k_decode     persistent wavefront decoder, one CTA per stream
+//                (codec.py:193-247, coder.py:76-112)
+//   k_forward_taps / k_channel_cdfs / k_rc_decode_tables  parity seams
+#include "../../include/lpic_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "lpic_cdf.cuh"
+#include "lpic_math.cuh"
+#include "lpic_net.cuh"
+#include "lpic_rc.cuh"
+#include "lpic_sched.cuh"
+
+using namespace lpic;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return fail(LPIC_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+    } while (0)
+
+constexpr int NET_THREADS = 128;   // pixels per CTA tile (encoder) / per decoder chunk
+
+
+struct LdgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldg(p); } };
+struct LdcgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldcg(p); } };
+
+__device__ __forceinline__ void init_consts(float* lut, double* edges) {
+    for (int v = threadIdx.x; v < 256; v += blockDim.x)
+        lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);            // network.py:172-177
+    for (int k = threadIdx.x; k < 257; k += blockDim.x)
+        edges[k] = __ddiv_rn(2.0 * (double)k - 256.0, 255.0);            // kernels.py:34
+}
+
+template <int CP>
+__host__ __device__ constexpr size_t net_smem_bytes(int MP) {
+    return (size_t)NET_THREADS * MP * sizeof(float) + (size_t)CP * NET_THREADS * sizeof(float);
+}
+
+// write the warp-held table as an int32 cdf[257] row
+__device__ __forceinline__ void store_cdf_row(int32_t* row, const uint32_t start[8], const uint32_t mass[8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 8; q++) row[8 * lane + q] = (int32_t)start[q];
+    if (lane == 31) row[256] = (int32_t)(start[7] + mass[7]);
+}
+
+// ---------------------------------------------------------------------------
+// encoder: network + tables for 128 pixels (coding order) per CTA
+// ---------------------------------------------------------------------------
+template <int CP, int HH>
+__global__ void __launch_bounds__(NET_THREADS)
+k_encode(NetDev w, int K, int dist, const uint8_t* __restrict__ images, int H, int W, int mode,
+         const int32_t* __restrict__ order, int64_t N, uint32_t* __restrict__ sw, int32_t* status,
+         float* trace_raw, int32_t* trace_cdf) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* edges = reinterpret_cast<double*>(smem);                                   // 257
+    float* lut = reinterpret_cast<float*>(smem + 257 * 8 + 8);                          // 256
+    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + 257 * 8 + 8 + 1024);  // 4
+    float* raw = reinterpret_cast<float*>(smem + 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch));
+    float* zbuf = raw + NET_THREADS * w.MP;
+
+    init_consts(lut, edges);
+    __syncthreads();
+    const int img = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int64_t n0 = (int64_t)blockIdx.x * NET_THREADS;
+    const uint8_t* im = images + (int64_t)img * N * 3;
+    const int64_t n = n0 + tid;
+    if (n < N) {
+        const int32_t ij = __ldg(order + n);
+        const int i = ij >> 16, j = ij & 0xFFFF;
+        float x[Taps<HH>::TC];
+        gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdgU8());
+        float* r = raw + tid * w.MP;
+        net_forward<CP, Taps<HH>::TC>(w, x, r, zbuf + tid, NET_THREADS);
+        bool finite = true;
+        for (int m = 0; m < w.M; m++) finite &= isfinite(r[m]);
+        if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
+        if (trace_raw)
+            for (int m = 0; m < w.M; m++) trace_raw[((int64_t)img * N + n) * w.M + m] = r[m];
+    }
+    __syncthreads();
+    const int wid = tid >> 5, lane = tid & 31;
+    const int cnt = (int)((N - n0) < NET_THREADS ? (N - n0) : NET_THREADS);
+    for (int p = wid * 32; p < min(cnt, wid * 32 + 32); p++) {
+        const int64_t nn = n0 + p;
+        const int32_t ij = __ldg(order + nn);
+        const int i = ij >> 16, j = ij & 0xFFFF;
+        const uint8_t* px = im + ((int64_t)i * W + j) * 3;
+        const int s0 = __ldg(px), s1 = __ldg(px + 1), s2 = __ldg(px + 2);
+        const float rn = lut[s0], gn = lut[s1];
+#pragma unroll 1
+        for (int ch = 0; ch < 3; ch++) {
+            uint32_t start[8], mass[8];
+            warp_table(raw + p * w.MP, K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, edges, sc + wid,
+                       start, mass);
+            const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
+            if (lane == (sym >> 3)) {
+                uint32_t st = 0, ms = 1;
+#pragma unroll
+                for (int q = 0; q < 8; q++) if (q == (sym & 7)) { st = start[q]; ms = mass[q]; }
+                sw[((int64_t)img * N + nn) * 3 + ch] = (st << 16) | (ms - 1);
+            }
+            if (trace_cdf) store_cdf_row(trace_cdf + (((int64_t)img * N + nn) * 3 + ch) * 257, start, mass);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// range-coder lanes: one warp per stream, every lane runs the same state,
+// lane 0 writes.  sw entry = start<<16 | (width-1).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32)
+k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
+            int64_t fixed_cnt, uint8_t* out, int64_t cap_each, int64_t* lens, int32_t* status) {
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
+    const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    RcEncoder e;
+    e.init(out + (int64_t)s * cap_each, cap_each);
+    uint32_t nxt = (lane < n) ? __ldg(sw + base + lane) : 0u;
+    for (int64_t c = 0; c < n; c += 32) {
+        const uint32_t v = nxt;
+        nxt = (c + 32 + lane < n) ? __ldg(sw + base + c + 32 + lane) : 0u;
+        const int m = (int)((n - c) < 32 ? (n - c) : 32);
+        for (int q = 0; q < m; q++) {
+            const uint32_t x = __shfl_sync(0xffffffffu, v, q);
+            e.encode(x >> 16, (x & 0xFFFFu) + 1u, lane == 0);
+        }
+    }
+    const int64_t len = e.finish(lane == 0);
+    if (lane == 0) {
+        lens[s] = len;
+        if (e.status) atomicOr(status + s, e.status);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// wavefront decoder: one CTA per stream.  Per step: all pixels of the step
+// evaluate the network in parallel (their taps are decoded), then warp 0
+// runs the serial r -> g -> b chain (codec.py:218-246).
+// ---------------------------------------------------------------------------
+template <int CP, int HH>
+__global__ void __launch_bounds__(NET_THREADS)
+k_decode(NetDev w, int K, int dist, const uint8_t* __restrict__ payload, const int64_t* __restrict__ offs,
+         const int64_t* __restrict__ lens, int H, int W, int mode, uint8_t* images, int32_t* status,
+         float* trace_raw, int32_t* trace_cdf) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* edges = reinterpret_cast<double*>(smem);
+    float* lut = reinterpret_cast<float*>(smem + 257 * 8 + 8);
+    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + 257 * 8 + 8 + 1024);
+    float* raw = reinterpret_cast<float*>(smem + 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch));
+    float* zbuf = raw + NET_THREADS * w.MP;
+    __shared__ int s_stop;
+
+    init_consts(lut, edges);
+    if (threadIdx.x == 0) s_stop = 0;
+    __syncthreads();
+    const int img = blockIdx.x, tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    const int64_t N = (int64_t)H * W;
+    uint8_t* im = images + (int64_t)img * N * 3;
+    const int a = sched_a(mode, W, HH);
+    const int64_t steps = sched_steps(mode, H, W, HH);
+    RcDecoder dec;
+    if (wid == 0) dec.init(payload + offs[img], lens[img]);
+    int64_t done = 0;
+    for (int64_t t = 0; t < steps; t++) {
+        int i_lo, i_hi;
+        sched_rows(t, a, H, W, i_lo, i_hi);
+        const int cnt = i_hi - i_lo + 1;
+        if (cnt <= 0) continue;
+        for (int c0 = 0; c0 < cnt; c0 += NET_THREADS) {
+            const int nb = min(NET_THREADS, cnt - c0);
+            if (tid < nb) {
+                const int i = i_lo + c0 + tid;
+                const int j = (int)(t - (int64_t)a * i);
+                float x[Taps<HH>::TC];
+                gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdcgU8());
+                net_forward<CP, Taps<HH>::TC>(w, x, raw + tid * w.MP, zbuf + tid, NET_THREADS);
+            }
+            __syncthreads();
+            if (wid == 0) {
+                for (int p = 0; p < nb; p++) {
+                    const int i = i_lo + c0 + p;
+                    const int j = (int)(t - (int64_t)a * i);
+                    const float* r = raw + p * w.MP;
+                    const int64_t n = done + c0 + p;
+                    if (trace_raw)
+                        for (int m = lane; m < w.M; m += 32) trace_raw[((int64_t)img * N + n) * w.M + m] = r[m];
+                    float rn = 0.0f, gn = 0.0f;
+                    int sym[3];
+#pragma unroll 1
+                    for (int ch = 0; ch < 3; ch++) {
+                        uint32_t start[8], mass[8];
+                        warp_table(r, K, dist, ch, rn, gn, edges, sc, start, mass);
+                        uint64_t rr;
+                        const uint32_t target = dec.target(rr);
+                        uint32_t s_st, s_ms;
+                        sym[ch] = warp_find_symbol(start, target, s_st, s_ms, mass);
+                        dec.advance(rr, s_st, s_ms);
+                        if (trace_cdf) store_cdf_row(trace_cdf + (((int64_t)img * N + n) * 3 + ch) * 257, start, mass);
+                        if (ch == 0) rn = lut[sym[0]];
+                        if (ch == 1) gn = lut[sym[1]];
+                    }
+                    if (lane == 0) {
+                        uint8_t* px = im + ((int64_t)i * W + j) * 3;
+                        px[0] = (uint8_t)sym[0]; px[1] = (uint8_t)sym[1]; px[2] = (uint8_t)sym[2];
+                    }
+                }
+                if (lane == 0 && dec.status) s_stop = 1;
+            }
+            __syncthreads();
+            if (s_stop) break;
+        }
+        if (s_stop) break;
+        done += cnt;
+    }
+    if (tid == 0 && dec.status) atomicOr(status + img, dec.status);
+}
+
+// ---------------------------------------------------------------------------
+// parity seams
+// ---------------------------------------------------------------------------
+template <int CP, int HH>
+__global__ void __launch_bounds__(NET_THREADS)
+k_forward_taps(NetDev w, const float* __restrict__ taps, int64_t N, float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* raw = reinterpret_cast<float*>(smem);
+    float* zbuf = raw + NET_THREADS * w.MP;
+    const int64_t n = (int64_t)blockIdx.x * NET_THREADS + threadIdx.x;
+    if (n >= N) return;
+    float x[Taps<HH>::TC];
+#pragma unroll
+    for (int k = 0; k < Taps<HH>::TC; k++) x[k] = taps[n * Taps<HH>::TC + k];
+    float* r = raw + threadIdx.x * w.MP;
+    net_forward<CP, Taps<HH>::TC>(w, x, r, zbuf + threadIdx.x, NET_THREADS);
+    for (int m = 0; m < w.M; m++) out[n * w.M + m] = r[m];
+}
+
+template <int CP, int HH>
+__global__ void __launch_bounds__(NET_THREADS)
+k_forward_full(NetDev w, const float* __restrict__ plane, int H, int W, float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* raw = reinterpret_cast<float*>(smem);
+    float* zbuf = raw + NET_THREADS * w.MP;
+    const int64_t n = (int64_t)blockIdx.x * NET_THREADS + threadIdx.x;
+    if (n >= (int64_t)H * W) return;
+    const int i = (int)(n / W), j = (int)(n % W);
+    float x[Taps<HH>::TC];
+#pragma unroll
+    for (int k = 0; k < Taps<HH>::T; k++) {
+        const int ii = i + Taps<HH>::di(k), jj = j + Taps<HH>::dj(k);
+        const bool in = ii >= 0 && ii < H && jj >= 0 && jj < W;
+        for (int c = 0; c < 3; c++) x[3 * k + c] = in ? plane[((int64_t)ii * W + jj) * 3 + c] : 0.0f;
+    }
+    float* r = raw + threadIdx.x * w.MP;
+    net_forward<CP, Taps<HH>::TC>(w, x, r, zbuf + threadIdx.x, NET_THREADS);
+    for (int m = 0; m < w.M; m++) out[n * w.M + m] = r[m];
+}
+
+__global__ void __launch_bounds__(128)
+k_channel_cdfs(const float* __restrict__ raw, int64_t N, int M, int K, int dist, int ch,
+               const float* __restrict__ rn, const float* __restrict__ gn, int32_t* __restrict__ out) {
+    __shared__ double edges[257];
+    __shared__ float lut[256];
+    __shared__ WarpCdfScratch sc[4];
+    init_consts(lut, edges);
+    __syncthreads();
+    const int wid = threadIdx.x >> 5;
+    const int64_t n = (int64_t)blockIdx.x * 4 + wid;
+    if (n >= N) return;
+    uint32_t start[8], mass[8];
+    warp_table(raw + n * M, K, dist, ch, rn[n], gn[n], edges, sc + wid, start, mass);
+    store_cdf_row(out + n * 257, start, mass);
+}
+
+__global__ void k_rc_decode_tables(const uint8_t* data, int64_t len, const int32_t* cdf, int64_t N,
+                                   int32_t* syms, int32_t* status) {
+    RcDecoder d;
+    d.init(data, len);
+    for (int64_t n = 0; n < N && !d.status; n++) {
+        const int32_t* c = cdf + n * 257;
+        uint64_t r;
+        const uint32_t target = d.target(r);
+        int lo = 0, hi = 256;
+        while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if ((uint32_t)c[mid] <= target) lo = mid; else hi = mid; }
+        d.advance(r, (uint32_t)c[lo], (uint32_t)(c[lo + 1] - c[lo]));
+        syms[n] = lo;
+    }
+    *status = d.status;
+}
+
+// pack payloads of n streams (fixed stride) into one buffer at offs
+__global__ void k_pack(const uint8_t* src, int64_t cap_each, const int64_t* offs, const int64_t* lens,
+                       uint8_t* dst) {
+    const int s = blockIdx.y;
+    const int64_t L = lens[s];
+    const uint8_t* a = src + (int64_t)s * cap_each;
+    uint8_t* b = dst + offs[s];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < L; k += (int64_t)gridDim.x * blockDim.x)
+        b[k] = a[k];
+}
+
+}  // namespace
+
+// ===========================================================================
+// host side: the model handle and the C-ABI
+// ===========================================================================
+struct lpic_model {
+    int K, C, L, h, dist, M, T, TC, CP, MP, NH;
+    int device;
+    int precision;
+    uint64_t fingerprint;
+    float* d_w;          // one allocation for all padded tensors
+    NetDev net;
+    // cached coding order per geometry
+    int32_t* d_order = nullptr;
+    int ord_H = -1, ord_W = -1, ord_mode = -1;
+    // workspace
+    uint32_t* d_sw = nullptr; size_t sw_cap = 0;
+    uint8_t* d_img = nullptr; size_t img_cap = 0;
+    uint8_t* d_pay = nullptr; size_t pay_cap = 0;
+    uint8_t* d_pack = nullptr; size_t pack_cap = 0;
+    int64_t* d_meta = nullptr; size_t meta_cap = 0;   // lens | offs
+    int32_t* d_status = nullptr; size_t status_cap = 0;
+    int launches = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+template <typename T>
+int ensure(T*& p, size_t& cap, size_t need) {
+    if (need <= cap && p) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t n = need < 64 ? 64 : need;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return fail(LPIC_E_NOMEM, "cudaMalloc workspace failed");
+    cap = n;
+    return 0;
+}
+
+template <typename Kern>
+int set_smem(Kern k, size_t bytes) {
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return 0;
+}
+
+size_t table_smem() { return 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch); }
+
+int coding_order(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
+    if (m->d_order && m->ord_H == H && m->ord_W == W && m->ord_mode == mode) return 0;
+    const int64_t N = (int64_t)H * W;
+    std::vector<int32_t> ord((size_t)N);
+    const int a = sched_a(mode, W, m->h);
+    const int64_t steps = sched_steps(mode, H, W, m->h);
+    int64_t n = 0;
+    for (int64_t t = 0; t < steps; t++) {
+        int lo, hi;
+        sched_rows(t, a, H, W, lo, hi);
+        for (int i = lo; i <= hi; i++) ord[(size_t)n++] = (i << 16) | (int)(t - (int64_t)a * i);
+    }
+    if (m->d_order) cudaFree(m->d_order);
+    m->d_order = nullptr;
+    CUDA_TRY(cudaMalloc(&m->d_order, sizeof(int32_t) * N));
+    CUDA_TRY(cudaMemcpyAsync(m->d_order, ord.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    m->ord_H = H; m->ord_W = W; m->ord_mode = mode;
+    return 0;
+}
+
+// template dispatch on (CP, HH)
+template <template <int, int> class F, typename... A>
+int dispatch(int CP, int HH, A&&... args) {
+#define LPIC_CASE(cp, hh) if (CP == cp && HH == hh) return F<cp, hh>::run(args...);
+    LPIC_CASE(16, 1) LPIC_CASE(32, 1) LPIC_CASE(64, 1) LPIC_CASE(128, 1)
+    LPIC_CASE(16, 2) LPIC_CASE(32, 2) LPIC_CASE(64, 2) LPIC_CASE(128, 2)
+    LPIC_CASE(16, 3) LPIC_CASE(32, 3) LPIC_CASE(64, 3) LPIC_CASE(128, 3)
+#undef LPIC_CASE
+    return fail(LPIC_E_UNSUPPORTED, "unsupported (C, kernel_half) instantiation");
+}
+
+template <int CP, int HH> struct EncodeRun {
+    static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, uint32_t* sw,
+                   int32_t* d_status, float* tr, int32_t* tc, cudaStream_t st) {
+        const size_t smem = table_smem() + net_smem_bytes<CP>(m->MP);
+        if (set_smem(k_encode<CP, HH>, smem)) return LPIC_E_CUDA;
+        const int64_t N = (int64_t)H * W;
+        dim3 grid((unsigned)((N + NET_THREADS - 1) / NET_THREADS), (unsigned)n);
+        k_encode<CP, HH><<<grid, NET_THREADS, smem, st>>>(m->net, m->K, m->dist, d_images, H, W, mode, m->d_order,
+                                                           N, sw, d_status, tr, tc);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+};
+
+template <int CP, int HH> struct DecodeRun {
+    static int run(lpic_model* m, const uint8_t* d_payload, const int64_t* d_offs, const int64_t* d_lens, int n,
+                   int H, int W, int mode, uint8_t* d_images, int32_t* d_status, float* tr, int32_t* tc,
+                   cudaStream_t st) {
+        const size_t smem = table_smem() + net_smem_bytes<CP>(m->MP);
+        if (set_smem(k_decode<CP, HH>, smem)) return LPIC_E_CUDA;
+        k_decode<CP, HH><<<n, NET_THREADS, smem, st>>>(m->net, m->K, m->dist, d_payload, d_offs, d_lens, H, W, mode,
+                                                        d_images, d_status, tr, tc);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+};
+
+template <int CP, int HH> struct TapsRun {
+    static int run(lpic_model* m, const float* taps, int64_t N, float* out, cudaStream_t st) {
+        const size_t smem = net_smem_bytes<CP>(m->MP);
+        if (set_smem(k_forward_taps<CP, HH>, smem)) return LPIC_E_CUDA;
+        k_forward_taps<CP, HH><<<(unsigned)((N + NET_THREADS - 1) / NET_THREADS), NET_THREADS, smem, st>>>(
+            m->net, taps, N, out);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+};
+
+template <int CP, int HH> struct FullRun {
+    static int run(lpic_model* m, const float* plane, int H, int W, float* out, cudaStream_t st) {
+        const size_t smem = net_smem_bytes<CP>(m->MP);
+        if (set_smem(k_forward_full<CP, HH>, smem)) return LPIC_E_CUDA;
+        const int64_t N = (int64_t)H * W;
+        k_forward_full<CP, HH><<<(unsigned)((N + NET_THREADS - 1) / NET_THREADS), NET_THREADS, smem, st>>>(
+            m->net, plane, H, W, out);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+};
+
+int check_geom(const lpic_model* m, int n, int H, int W, int mode) {
+    if (!m) return fail(LPIC_E_ARG, "null model");
+    if (n < 0 || H < 1 || W < 1 || H > 32767 || W > 65535) return fail(LPIC_E_ARG, "bad image geometry");
+    if (mode < 0 || mode > 2) return fail(LPIC_E_ARG, "bad schedule mode");
+    if (mode == 2 && m->h != 2) return fail(LPIC_E_ARG, "diagonal schedule is only defined for kernel_half=2");
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lpic_version(void) { return 1; }
+const char* lpic_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t lpic_fnv1a64(const uint8_t* data, int64_t n) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (int64_t i = 0; i < n; i++) { h ^= data[i]; h *= 0x100000001b3ull; }
+    return h;
+}
+
+int lpic_model_create(const float* masked_w, const float* masked_b, const float* hidden_w, const float* hidden_b,
+                      const float* out_w, const float* out_b, int K, int C, int L, int h, int dist,
+                      lpic_model_t** out) {
+    if (!out || !masked_w || !masked_b || !out_w || !out_b || (L > 2 && (!hidden_w || !hidden_b)))
+        return fail(LPIC_E_ARG, "null argument");
+    if (K < 1 || K > KMAX) return fail(LPIC_E_UNSUPPORTED, "mixtures must be in [1, 16] on the GPU");
+    if (C < 1 || C > 128) return fail(LPIC_E_UNSUPPORTED, "filters must be in [1, 128] on the GPU");
+    if (L < 3) return fail(LPIC_E_ARG, "need at least 3 layers");
+    if (h < 1 || h > 3) return fail(LPIC_E_UNSUPPORTED, "kernel_half must be 1, 2 or 3 on the GPU");
+    if (dist != 0 && dist != 1) return fail(LPIC_E_ARG, "unknown distribution");
+    lpic_model* m = new lpic_model();
+    m->K = K; m->C = C; m->L = L; m->h = h; m->dist = dist;
+    m->M = 12 * K; m->T = (2 * h + 1) * h + h; m->TC = 3 * m->T;
+    m->CP = C <= 16 ? 16 : C <= 32 ? 32 : C <= 64 ? 64 : 128;
+    m->MP = (m->M + 3) & ~3;
+    m->NH = L - 2;
+    m->precision = LPIC_PREC_COMPAT;
+    cudaGetDevice(&m->device);
+    const int CP = m->CP, MP = m->MP, NH = m->NH, T = m->T, TC = m->TC, M = m->M;
+    // padded host layouts
+    std::vector<float> mwT((size_t)CP * TC, 0.f), mb(CP, 0.f), hw((size_t)NH * CP * CP, 0.f), hb((size_t)NH * CP, 0.f),
+        ow((size_t)MP * CP, 0.f), ob(MP, 0.f);
+    for (int t = 0; t < T; t++)
+        for (int c = 0; c < 3; c++)
+            for (int f = 0; f < C; f++) mwT[(size_t)f * TC + t * 3 + c] = masked_w[(t * 3 + c) * C + f];
+    for (int f = 0; f < C; f++) mb[f] = masked_b[f];
+    for (int l = 0; l < NH; l++)
+        for (int o = 0; o < C; o++) {
+            for (int i = 0; i < C; i++) hw[((size_t)l * CP + o) * CP + i] = hidden_w[((size_t)l * C + o) * C + i];
+            hb[(size_t)l * CP + o] = hidden_b[(size_t)l * C + o];
+        }
+    for (int mm = 0; mm < M; mm++) {
+        for (int i = 0; i < C; i++) ow[(size_t)mm * CP + i] = out_w[(size_t)mm * C + i];
+        ob[mm] = out_b[mm];
+    }
+    const size_t total = mwT.size() + mb.size() + hw.size() + hb.size() + ow.size() + ob.size();
+    if (cudaMalloc(&m->d_w, total * sizeof(float)) != cudaSuccess) { delete m; return fail(LPIC_E_NOMEM, "cudaMalloc weights"); }
+    float* p = m->d_w;
+    auto put = [&](const std::vector<float>& v) -> const float* {
+        cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice);
+        const float* r = p;
+        p += v.size();
+        return r;
+    };
+    m->net.mwT = put(mwT); m->net.mb = put(mb); m->net.hw = put(hw); m->net.hb = put(hb);
+    m->net.ow = put(ow); m->net.ob = put(ob);
+    m->net.C = C; m->net.CP = CP; m->net.M = M; m->net.MP = MP; m->net.NH = NH; m->net.T = T; m->net.TC = TC;
+    // fingerprint of the LPWT serialisation (network.py:255-281)
+    std::vector<uint8_t> ser;
+    const char magic[4] = {'L', 'P', 'W', 'T'};
+    ser.insert(ser.end(), magic, magic + 4);
+    const uint8_t hdr[6] = {1, (uint8_t)K, (uint8_t)C, (uint8_t)L, (uint8_t)h, (uint8_t)dist};
+    ser.insert(ser.end(), hdr, hdr + 6);
+    auto app = [&](const float* src, size_t count) {
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(src);
+        ser.insert(ser.end(), b, b + count * 4);
+    };
+    app(masked_w, (size_t)T * 3 * C); app(masked_b, C);
+    app(hidden_w, (size_t)NH * C * C); app(hidden_b, (size_t)NH * C);
+    app(out_w, (size_t)M * C); app(out_b, M);
+    m->fingerprint = lpic_fnv1a64(ser.data(), (int64_t)ser.size());
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { cudaFree(m->d_w); delete m; return fail(LPIC_E_CUDA, cudaGetErrorString(e)); }
+    *out = m;
+    return 0;
+}
+
+int lpic_model_destroy(lpic_model_t* m) {
+    if (!m) return 0;
+    cudaFree(m->d_w);
+    cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_img); cudaFree(m->d_pay);
+    cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
+    delete m;
+    return 0;
+}
+
+int lpic_model_set_precision(lpic_model_t* m, int precision) {
+    if (!m) return fail(LPIC_E_ARG, "null model");
+    if (precision != LPIC_PREC_COMPAT) return fail(LPIC_E_UNSUPPORTED, "only LPIC_PREC_COMPAT is built in this version");
+    m->precision = precision;
+    return 0;
+}
+
+uint64_t lpic_model_fingerprint(const lpic_model_t* m) { return m ? m->fingerprint : 0; }
+int lpic_last_launch_count(const lpic_model_t* m) { return m ? m->launches : 0; }
+
+int lpic_forward_taps(lpic_model_t* m, const float* d_taps, int64_t N, float* d_raw, void* stream) {
+    if (!m || N < 0) return fail(LPIC_E_ARG, "bad argument");
+    if (N == 0) return 0;
+    return dispatch<TapsRun>(m->CP, m->h, m, d_taps, N, d_raw, (cudaStream_t)stream);
+}
+
+int lpic_forward_full(lpic_model_t* m, const float* d_plane, int H, int W, float* d_raw, void* stream) {
+    if (!m || H < 1 || W < 1) return fail(LPIC_E_ARG, "bad argument");
+    return dispatch<FullRun>(m->CP, m->h, m, d_plane, H, W, d_raw, (cudaStream_t)stream);
+}
+
+int lpic_channel_cdfs(const float* d_raw, int64_t N, int M, int K, int dist, int channel, const float* d_rn,
+                      const float* d_gn, int32_t* d_cdf, void* stream) {
+    if (N < 0 || K < 1 || K > KMAX || M < 12 * K || channel < 0 || channel > 2) return fail(LPIC_E_ARG, "bad argument");
+    if (N == 0) return 0;
+    k_channel_cdfs<<<(unsigned)((N + 3) / 4), 128, 0, (cudaStream_t)stream>>>(d_raw, N, M, K, dist, channel, d_rn, d_gn,
+                                                                             d_cdf);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt, int n_streams,
+                           uint8_t* d_out, int64_t cap_each, int64_t* d_len, int32_t* d_status, void* stream) {
+    if (n_streams < 0 || !d_off || !d_cnt) return fail(LPIC_E_ARG, "bad argument");
+    if (n_streams == 0) return 0;
+    k_rc_encode<<<n_streams, 32, 0, (cudaStream_t)stream>>>(d_sw, d_off, d_cnt, 0, d_out, cap_each, d_len, d_status);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_cdf, int64_t N, int32_t* d_syms,
+                          int32_t* d_status, void* stream) {
+    if (N < 0 || len < 0) return fail(LPIC_E_ARG, "bad argument");
+    k_rc_decode_tables<<<1, 1, 0, (cudaStream_t)stream>>>(d_data, len, d_cdf, N, d_syms, d_status);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode,
+                             uint8_t* d_payload, int64_t cap_each, int64_t* d_lens, int32_t* d_status,
+                             float* d_trace_raw, int32_t* d_trace_cdf, void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lk(m->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = (int64_t)H * W;
+    if (int r = coding_order(m, H, W, mode, st)) return r;
+    if (int r = ensure(m->d_sw, m->sw_cap, (size_t)n * N * 3)) return r;
+    CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
+    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_sw, d_status, d_trace_raw,
+                                    d_trace_cdf, st))
+        return r;
+    k_rc_encode<<<n, 32, 0, st>>>(m->d_sw, nullptr, nullptr, 3 * N, d_payload, cap_each, d_lens, d_status);
+    CUDA_TRY(cudaGetLastError());
+    m->launches = 2;
+    return 0;
+}
+
+int lpic_decode_batch_device(lpic_model_t* m, const uint8_t* d_payload, const int64_t* d_offs, const int64_t* d_lens,
+                             int n, int H, int W, int mode, uint8_t* d_images, int32_t* d_status, float* d_trace_raw,
+                             int32_t* d_trace_cdf, void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lk(m->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
+    CUDA_TRY(cudaMemsetAsync(d_images, 0, (size_t)n * H * W * 3, st));
+    if (int r = dispatch<DecodeRun>(m->CP, m->h, m, d_payload, d_offs, d_lens, n, H, W, mode, d_images, d_status,
+                                    d_trace_raw, d_trace_cdf, st))
+        return r;
+    m->launches = 1;
+    return 0;
+}
+
+int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, int W, int mode, uint8_t* h_payload,
+                      int64_t payload_cap, int64_t* h_offs, int64_t* h_lens, int32_t* h_status, void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = (int64_t)H * W;
+    const int64_t cap_each = 6 * N + 64;
+    {
+        std::lock_guard<std::mutex> lk(m->mu);
+        if (int r = ensure(m->d_img, m->img_cap, (size_t)n * N * 3)) return r;
+        if (int r = ensure(m->d_pay, m->pay_cap, (size_t)n * cap_each)) return r;
+        if (int r = ensure(m->d_meta, m->meta_cap, (size_t)2 * n)) return r;
+        if (int r = ensure(m->d_status, m->status_cap, (size_t)n)) return r;
+        CUDA_TRY(cudaMemcpyAsync(m->d_img, h_images, (size_t)n * N * 3, cudaMemcpyHostToDevice, st));
+    }
+    if (int r = lpic_encode_batch_device(m, m->d_img, n, H, W, mode, m->d_pay, cap_each, m->d_meta, m->d_status,
+                                         nullptr, nullptr, stream))
+        return r;
+    std::lock_guard<std::mutex> lk(m->mu);
+    CUDA_TRY(cudaMemcpyAsync(h_lens, m->d_meta, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_status, m->d_status, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t total = 0;
+    for (int b = 0; b < n; b++) { h_offs[b] = total; total += h_lens[b] > cap_each ? cap_each : h_lens[b]; }
+    if (total > payload_cap) return fail(LPIC_E_ARG, "h_payload capacity too small (lens filled)");
+    if (int r = ensure(m->d_pack, m->pack_cap, (size_t)total)) return r;
+    CUDA_TRY(cudaMemcpyAsync(m->d_meta + n, h_offs, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+    k_pack<<<dim3(64, n), 256, 0, st>>>(m->d_pay, cap_each, m->d_meta + n, m->d_meta, m->d_pack);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h_payload, m->d_pack, (size_t)total, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    m->launches = 3;
+    return 0;
+}
+
+int lpic_decode_batch(lpic_model_t* m, const uint8_t* h_payload, const int64_t* h_offs, const int64_t* h_lens, int n,
+                      int H, int W, int mode, uint8_t* h_images, int32_t* h_status, void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = (int64_t)H * W;
+    int64_t total = 0;
+    for (int b = 0; b < n; b++) total = h_offs[b] + h_lens[b] > total ? h_offs[b] + h_lens[b] : total;
+    {
+        std::lock_guard<std::mutex> lk(m->mu);
+        if (int r = ensure(m->d_img, m->img_cap, (size_t)n * N * 3)) return r;
+        if (int r = ensure(m->d_pack, m->pack_cap, (size_t)total + 8)) return r;
+        if (int r = ensure(m->d_meta, m->meta_cap, (size_t)2 * n)) return r;
+        if (int r = ensure(m->d_status, m->status_cap, (size_t)n)) return r;
+        CUDA_TRY(cudaMemcpyAsync(m->d_pack, h_payload, (size_t)total, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(m->d_meta, h_offs, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(m->d_meta + n, h_lens, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+    }
+    if (int r = lpic_decode_batch_device(m, m->d_pack, m->d_meta, m->d_meta + n, n, H, W, mode, m->d_img, m->d_status,
+                                         nullptr, nullptr, stream))
+        return r;
+    std::lock_guard<std::mutex> lk(m->mu);
+    CUDA_TRY(cudaMemcpyAsync(h_images, m->d_img, (size_t)n * N * 3, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_status, m->d_status, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// lpic_rc.cuh -- 48-bit range coder lanes, byte-compatible with the
+// reference RangeEncoder / RangeDecoder (/root/reference/pkg/src/lpic/coder.py:22-112).
+//
+// The encoder keeps the reference's carry semantics without random access
+// to already-written output: the emitted stream is F ++ [cache] ++ [0xFF]*nff
+// where F is final, `cache` is the last byte a carry can still increment and
+// the trailing 0xFF run is what coder.py:52-57 would zero on a carry.  This
+// is exactly the reference's byte array, produced strictly sequentially.
+#pragma once
+#include <cstdint>
+
+namespace lpic {
+
+constexpr uint64_t RC_TOP = 1ull << 48;
+constexpr uint64_t RC_BOTTOM = 1ull << 40;
+constexpr uint64_t RC_MASK = RC_TOP - 1;
+
+enum : int { ST_OK = 0, ST_NONFINITE = 1, ST_CORRUPT = 2, ST_CAPACITY = 4, ST_ARG = 8 };
+
+struct RcEncoder {
+    uint64_t low, range;
+    uint8_t* out;
+    int64_t pos, cap;
+    uint32_t nff;
+    int cache;        // -1: no byte emitted yet
+    int status;
+
+    __device__ __forceinline__ void init(uint8_t* o, int64_t c) {
+        low = 0; range = RC_TOP - 1; out = o; pos = 0; cap = c; nff = 0; cache = -1; status = ST_OK;
+    }
+    __device__ __forceinline__ void put(int b, bool writer) {
+        if (pos < cap) { if (writer) out[pos] = (uint8_t)b; }
+        else status |= ST_CAPACITY;
+        pos++;
+    }
+    __device__ __forceinline__ void emit(int b, bool writer) {
+        if (cache < 0) { cache = b; return; }
+        if (b == 0xFF) { nff++; return; }
+        put(cache, writer);
+        for (; nff; nff--) put(0xFF, writer);
+        cache = b;
+    }
+    __device__ __forceinline__ void carry(bool writer) {   // coder.py:52-57
+        if (nff) {
+            put(cache + 1, writer);
+            for (uint32_t q = 1; q < nff; q++) put(0x00, writer);
+            cache = 0x00;
+            nff = 0;
+        } else {
+            cache += 1;
+        }
+    }
+    // coder.py:37-50
+    __device__ __forceinline__ void encode(uint32_t start, uint32_t width, bool writer) {
+        const uint64_t r = range >> 16;
+        low += r * start;
+        range = r * width;
+        if (low >= RC_TOP) { low -= RC_TOP; carry(writer); }
+        while (range < RC_BOTTOM) {
+            emit((int)((low >> 40) & 0xFF), writer);
+            low = (low << 8) & RC_MASK;
+            range <<= 8;
+        }
+    }
+    // coder.py:59-73
+    __device__ __forceinline__ int64_t finish(bool writer) {
+        uint64_t value = ((low + (1ull << 24) - 1) >> 24) << 24;
+        if (value >= RC_TOP) { value -= RC_TOP; carry(writer); }
+        for (int k = 0; k < 3; k++) emit((int)((value >> (40 - 8 * k)) & 0xFF), writer);
+        if (cache >= 0) put(cache, writer);
+        for (; nff; nff--) put(0xFF, writer);
+        return pos;
+    }
+};
+
+struct RcDecoder {
+    uint64_t code, range;
+    const uint8_t* data;
+    int64_t len, pos;
+    int virt;
+    int status;
+
+    __device__ __forceinline__ int next_byte() {           // coder.py:86-96
+        if (pos < len) return __ldg(data + pos++);
+        virt++;
+        if (virt > 3) status |= ST_CORRUPT;
+        return 0;
+    }
+    __device__ __forceinline__ void init(const uint8_t* d, int64_t n) {
+        data = d; len = n; pos = 0; virt = 0; status = ST_OK; range = RC_TOP - 1; code = 0;
+        for (int k = 0; k < 6; k++) code = (code << 8) | (uint64_t)next_byte();
+    }
+    // target = min(code // r, 65535) (coder.py:100-103), exact via a float64
+    // quotient (code < 2^48, r < 2^32) and one integer correction.
+    __device__ __forceinline__ uint32_t target(uint64_t& r_out) const {
+        const uint64_t r = range >> 16;
+        uint64_t q = (uint64_t)__ddiv_rz((double)code, (double)r);
+        if (q * r > code) q--;
+        else if ((q + 1) * r <= code) q++;
+        r_out = r;
+        return q > 65535 ? 65535u : (uint32_t)q;
+    }
+    __device__ __forceinline__ void advance(uint64_t r, uint32_t start, uint32_t width) {   // coder.py:107-111
+        code -= r * start;
+        range = r * width;
+        while (range < RC_BOTTOM) {
+            code = ((code << 8) & RC_MASK) | (uint64_t)next_byte();
+            range <<= 8;
+        }
+    }
+};
+
+}  // namespace lpic

@@ -1,0 +1,91 @@
+// lpic_sched.cuh -- decoding schedules and causal-context gathers on device.
+//
+// All three reference schedules (/root/reference/pkg/src/lpic/schedules.py:72-133)
+// are linear: pixel (i,j) is decoded at step a*i + j with a = W (sequential),
+// h+1 (wavefront) or 1 (diagonal); inside a step pixels go in ascending i
+// (raster) order, which is the bitstream order (schedules.py:1-9).
+#pragma once
+#include <cstdint>
+
+namespace lpic {
+
+__host__ __device__ __forceinline__ int sched_a(int mode, int W, int h) {
+    return mode == 0 ? W : (mode == 1 ? h + 1 : 1);
+}
+__host__ __device__ __forceinline__ int64_t sched_steps(int mode, int H, int W, int h) {
+    return (int64_t)sched_a(mode, W, h) * (H - 1) + W;
+}
+// rows of step t: [i_lo, i_hi] (empty if i_lo > i_hi)
+__host__ __device__ __forceinline__ void sched_rows(int64_t t, int a, int H, int W, int& i_lo, int& i_hi) {
+    const int64_t lo_num = t - W + 1;
+    const int64_t lo = lo_num <= 0 ? 0 : (lo_num + a - 1) / a;
+    const int64_t hi = t / a;
+    i_lo = (int)lo;
+    i_hi = (int)(hi < H - 1 ? hi : H - 1);
+}
+
+template <int HH> struct Taps {
+    static constexpr int T = (2 * HH + 1) * HH + HH;
+    static constexpr int TC = 3 * T;
+    __host__ __device__ static constexpr int di(int k) { return k < (2 * HH + 1) * HH ? -HH + k / (2 * HH + 1) : 0; }
+    __host__ __device__ static constexpr int dj(int k) {
+        return k < (2 * HH + 1) * HH ? -HH + k % (2 * HH + 1) : -HH + (k - (2 * HH + 1) * HH);
+    }
+};
+
+// Causal taps of pixel (i,j) from a u8 image (zero padding outside;
+// kernels.py:101-108 / codec.py:93-96), normalised through `lut`.  In
+// diagonal mode the taps (-1,1), (-1,2), (-2,2) are redirected to (i-2,j+1)
+// or the first decoded in-bounds tap (schedules.py:114-131; h = 2 only).
+// LOAD(ptr) abstracts the load (L1-bypassing in the decoder).
+template <int HH, typename Load>
+__device__ __forceinline__ void gather_u8(const uint8_t* im, int H, int W, int i, int j, int mode,
+                                          const float* lut, float (&x)[Taps<HH>::TC], Load load) {
+    constexpr int T = Taps<HH>::T;
+#pragma unroll
+    for (int k = 0; k < T; k++) {
+        const int ii = i + Taps<HH>::di(k), jj = j + Taps<HH>::dj(k);
+        if (ii >= 0 && ii < H && jj >= 0 && jj < W) {
+            const uint8_t* p = im + ((int64_t)ii * W + jj) * 3;
+            x[3 * k + 0] = lut[load(p + 0)];
+            x[3 * k + 1] = lut[load(p + 1)];
+            x[3 * k + 2] = lut[load(p + 2)];
+        } else {
+            x[3 * k + 0] = 0.0f; x[3 * k + 1] = 0.0f; x[3 * k + 2] = 0.0f;
+        }
+    }
+    if constexpr (HH == 2) {
+        if (mode == 2) {
+            // source pixel: (i-2, j+1) if inside, else the first in-bounds tap on an
+            // earlier anti-diagonal in canonical order, else padding (None -> 0.0)
+            int si = i - 2, sj = j + 1;
+            bool found = (si >= 0 && si < H && sj >= 0 && sj < W);
+            if (!found) {
+#pragma unroll
+                for (int k = 0; k < T; k++) {
+                    const int ci = i + Taps<HH>::di(k), cj = j + Taps<HH>::dj(k);
+                    if (!found && ci >= 0 && ci < H && cj >= 0 && cj < W && Taps<HH>::di(k) + Taps<HH>::dj(k) < 0) {
+                        si = ci; sj = cj; found = true;
+                    }
+                }
+            }
+            float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f;
+            if (found) {
+                const uint8_t* p = im + ((int64_t)si * W + sj) * 3;
+                v0 = lut[load(p + 0)]; v1 = lut[load(p + 1)]; v2 = lut[load(p + 2)];
+            }
+            // tap indices of (-1,1)=8, (-1,2)=9, (-2,2)=4 in the h=2 canonical order
+            const int kk[3] = {8, 9, 4};
+#pragma unroll
+            for (int u = 0; u < 3; u++) {
+                const int k = kk[u];
+                const int ti = i + Taps<HH>::di(k), tj = j + Taps<HH>::dj(k);
+                if (ti >= 0 && ti < H && tj >= 0 && tj < W) {
+                    x[3 * k + 0] = v0; x[3 * k + 1] = v1; x[3 * k + 2] = v2;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace lpic
