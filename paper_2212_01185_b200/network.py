@@ -256,6 +256,7 @@ _MODELS: dict = {}
 
 def gpu_model(w: Weights, cfg: ModelConfig) -> GpuModel:
     import torch
+    _native.require_cuda()
     key = (weight_fingerprint(w, cfg), cfg, torch.cuda.current_device())
     m = _MODELS.get(key)
     if m is None:
