@@ -1,0 +1,328 @@
+// lpic_decode.cuh -- the wavefront decoder: one 2-CTA cluster per stream.
+//
+// Replaces codec.decode (/root/reference/pkg/src/lpic/codec.py:193-247) and
+// RangeDecoder (coder.py:76-112).  The per-stream work splits into
+//
+//   producer (cluster rank 1, 8 warps): for every pixel, in coding order, as
+//     soon as its causal taps are decoded: gather -> network (compat float32)
+//     -> red CDF table (warp builder) + the g/b mixture record (softmax
+//     weights, 1/s, base means, tanh coefficients).  Records go to a
+//     per-stream ring in global memory (L2-resident) with a ready flag each.
+//   consumer (cluster rank 0, 8 chain warps + 1 loader warp): the serial
+//     chain.  The loader bulk-copies record n (cp.async.bulk + mbarrier) into
+//     a 4-slot shared-memory ring; the chain decodes r from the red table,
+//     builds the green table (block builder, 256 threads), decodes g, builds
+//     blue, decodes b, writes the pixel and publishes its progress.
+//
+// Pixel (i,j) of step t is computable once pixel (i, j-1) -- the latest of
+// its taps in coding order, in step t-1 -- is decoded (all earlier steps
+// for j = 0), so the producer trails the chain by about one wavefront step
+// and its work is off the critical path.  The cluster guarantees both CTAs
+// are co-resident, so the cross-CTA spin-waits cannot deadlock.
+#pragma once
+#include "lpic_cdf.cuh"
+#include "lpic_net.cuh"
+#include "lpic_rc.cuh"
+#include "lpic_sched.cuh"
+
+namespace lpic {
+
+constexpr int DEC_CHAIN_THREADS = 256;
+constexpr int DEC_THREADS = 288;        // + loader warp (consumer) / idle warp (producer)
+constexpr int DEC_SLOTS = 4;
+
+struct DecParams {
+    NetDev w;
+    int K, dist, H, W, mode, a;
+    int64_t N;
+    const uint8_t* payload;
+    const int64_t* offs;
+    const int64_t* lens;
+    uint8_t* images;
+    int32_t* status;
+    const int32_t* order;        // coding index -> (i<<16)|j
+    const int64_t* step_off;     // steps+1 coding offsets
+    const int32_t* chunks;       // (n0, npx) pairs, each inside one step
+    int n_chunks;
+    uint8_t* ring;               // [n][ring][rec_bytes]
+    uint32_t* flags;             // [n][ring]
+    uint32_t* progress;          // [n]
+    int ring_size;               // power of two
+    int rec_bytes;
+    float* trace_raw;
+    int32_t* trace_cdf;
+};
+
+// record layout
+__host__ __device__ __forceinline__ int rec_mix_off() { return 512; }
+__host__ __device__ __forceinline__ int rec_bytes_for(int K) { return (512 + 32 * K + 20 * K + 15) & ~15; }
+struct RecView {
+    const uint16_t* red;   // cdf[0..255]
+    const double* pi_g; const double* inv_g; const double* pi_b; const double* inv_b;
+    const float* mu_g; const float* mu_b; const float* ta; const float* tb; const float* tc;
+    __device__ RecView(const unsigned char* r, int K) {
+        red = reinterpret_cast<const uint16_t*>(r);
+        const double* d = reinterpret_cast<const double*>(r + 512);
+        pi_g = d; inv_g = d + K; pi_b = d + 2 * K; inv_b = d + 3 * K;
+        const float* f = reinterpret_cast<const float*>(d + 4 * K);
+        mu_g = f; mu_b = f + K; ta = f + 2 * K; tb = f + 3 * K; tc = f + 4 * K;
+    }
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// producer
+// ---------------------------------------------------------------------------
+template <int CP, int HH>
+__device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
+    CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
+    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
+    float* raw = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch));
+    float* zbuf = raw + DEC_CHAIN_THREADS * P.w.MP;
+    load_consts(cc);
+    __syncthreads();
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    if (wid >= 8) return;
+    const int K = P.K;
+    const int64_t N = P.N;
+    const uint8_t* im = P.images + (int64_t)img * N * 3;
+    uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
+    uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
+    const uint32_t* progress = P.progress + img;
+    float* myraw = raw + tid * P.w.MP;
+    for (int c = wid; c < P.n_chunks; c += 8) {
+        const int n0 = P.chunks[2 * c], npx = P.chunks[2 * c + 1];
+        const int64_t n = n0 + lane;
+        const bool act = lane < npx;
+        int i = 0, j = 0;
+        int64_t req = 0;
+        if (act) {
+            const int32_t ij = __ldg(P.order + n);
+            i = ij >> 16; j = ij & 0xFFFF;
+            const int64_t t = (int64_t)P.a * i + j;
+            if (j >= 1) {
+                int lo, hi;
+                sched_rows(t - 1, P.a, P.H, P.W, lo, hi);
+                req = __ldg(P.step_off + t - 1) + (i - lo) + 1;
+            } else {
+                req = __ldg(P.step_off + t);
+            }
+        }
+        // also never run more than ring_size records ahead of the consumer
+        int64_t need = max(req, (int64_t)n0 + npx - P.ring_size);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+        if (lane == 0) {
+            uint32_t ns = 32;
+            while ((int64_t)ld_acquire_u32(progress) < need) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+        }
+        __syncwarp();
+        __threadfence();
+        if (act) {
+            float x[Taps<HH>::TC];
+            gather_u8<HH>(im, P.H, P.W, i, j, P.mode, cc->lut, x, LdcgU8());
+            net_forward<CP, Taps<HH>::TC>(P.w, x, myraw, zbuf + tid, DEC_CHAIN_THREADS);
+            if (P.trace_raw)
+                for (int m = 0; m < P.w.M; m++) P.trace_raw[((int64_t)img * N + n) * P.w.M + m] = myraw[m];
+            // g/b mixture record (kernels.py:212-247 minus the rn/gn-dependent update)
+            unsigned char* rec = ring + (int64_t)(n & (P.ring_size - 1)) * P.rec_bytes;
+            double* d = reinterpret_cast<double*>(rec + 512);
+            float* f = reinterpret_cast<float*>(d + 4 * K);
+            for (int q = 0; q < K; q++) {
+                d[q] = mix_pi(myraw, K, 1, q);
+                d[K + q] = mix_inv(myraw, K, 1, q);
+                d[2 * K + q] = mix_pi(myraw, K, 2, q);
+                d[3 * K + q] = mix_inv(myraw, K, 2, q);
+                f[q] = myraw[3 * K + 1 * K + q];
+                f[K + q] = myraw[3 * K + 2 * K + q];
+                f[2 * K + q] = tanhf_glibc(myraw[9 * K + q]);
+                f[3 * K + q] = tanhf_glibc(myraw[10 * K + q]);
+                f[4 * K + q] = tanhf_glibc(myraw[11 * K + q]);
+            }
+        }
+        __syncwarp();
+        // red tables, one warp-built table per pixel of the chunk
+        for (int p = 0; p < npx; p++) {
+            uint32_t start[8], mass[8];
+            warp_table(raw + (wid * 32 + p) * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
+            const int64_t np = n0 + p;
+            unsigned char* rec = ring + (int64_t)(np & (P.ring_size - 1)) * P.rec_bytes;
+            uint4 v;
+            v.x = (start[0] & 0xFFFFu) | (start[1] << 16); v.y = (start[2] & 0xFFFFu) | (start[3] << 16);
+            v.z = (start[4] & 0xFFFFu) | (start[5] << 16); v.w = (start[6] & 0xFFFFu) | (start[7] << 16);
+            reinterpret_cast<uint4*>(rec)[lane] = v;
+        }
+        __threadfence();
+        __syncwarp();
+        if (act) st_release_u32(flags + (n & (P.ring_size - 1)), (uint32_t)(n + 1));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// consumer: the serial chain
+// ---------------------------------------------------------------------------
+struct ConsumerSmem {
+    uint64_t full[DEC_SLOTS];
+    uint64_t empty[DEC_SLOTS];
+    BlockCdfScratch sc;
+};
+
+__device__ __forceinline__ void chain_symbol(BlockCdfScratch* sc, uint32_t start, uint32_t mass, uint32_t target) {
+    if (start <= target && target < start + mass) { sc->sym = threadIdx.x; sc->sstart = start; sc->smass = mass; }
+}
+
+__device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
+    CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
+    ConsumerSmem* cs = reinterpret_cast<ConsumerSmem*>(smem + sizeof(CdfConsts));
+    unsigned char* slots = smem + ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127);
+    load_consts(cc);
+    const int tid = threadIdx.x, wid = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&cs->full[s], 1); mbar_init(&cs->empty[s], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int K = P.K;
+    const int64_t N = P.N;
+    const uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
+    const uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
+    if (wid == 8) {                                   // loader warp
+        if ((tid & 31) == 0) {
+            for (int64_t n = 0; n < N; n++) {
+                const int s = (int)(n % DEC_SLOTS);
+                if (n >= DEC_SLOTS) mbar_wait(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1));
+                const uint32_t* fl = flags + (n & (P.ring_size - 1));
+                uint32_t ns = 32;
+                while (ld_acquire_u32(fl) != (uint32_t)(n + 1)) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                mbar_arrive_tx(&cs->full[s], (uint32_t)P.rec_bytes);
+                bulk_g2s(slots + s * P.rec_bytes, ring + (int64_t)(n & (P.ring_size - 1)) * P.rec_bytes,
+                         (uint32_t)P.rec_bytes, &cs->full[s]);
+            }
+        }
+        return;
+    }
+    uint8_t* im = P.images + (int64_t)img * N * 3;
+    RcDecoder dec;
+    dec.init(P.payload + P.offs[img], P.lens[img]);
+    BlockCdfScratch* sc = &cs->sc;
+    const double* pc = cc->phic;
+    for (int64_t n = 0; n < N; n++) {
+        const int s = (int)(n % DEC_SLOTS);
+        mbar_wait(&cs->full[s], (uint32_t)((n / DEC_SLOTS) & 1));
+        const RecView rv(slots + s * P.rec_bytes, K);
+        // ---- red: table precomputed by the producer
+        uint64_t r;
+        uint32_t target = dec.target(r);
+        const uint32_t rs = rv.red[tid];
+        const uint32_t re = tid == 255 ? 65536u : (uint32_t)rv.red[tid + 1];
+        chain_symbol(sc, rs, re - rs, target);
+        team_sync();
+        const int sr = sc->sym;
+        dec.advance(r, sc->sstart, sc->smass);
+        const float rn = cc->lut[sr];
+        // ---- green: mu_g += tanh(alpha)*rn (kernels.py:236-237)
+        double pmf = 0.0;
+        {
+            const int k = tid, lane = tid & 31;
+            for (int q = 0; q < K; q++) {
+                const double mu = (double)mu_update1(rv.mu_g[q], rv.ta[q], rn), inv = rv.inv_g[q];
+                const double cur = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k + 1], mu), inv), P.dist, pc);
+                double prev = __shfl_up_sync(0xffffffffu, cur, 1);
+                if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), inv), P.dist, pc);
+                const double d = __dsub_rn(cur, prev);
+                if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(rv.pi_g[q], d));
+            }
+        }
+        uint32_t gs, gm;
+        block_quantize(pmf, sc, gs, gm);
+        target = dec.target(r);
+        chain_symbol(sc, gs, gm, target);
+        team_sync();
+        const int sg = sc->sym;
+        dec.advance(r, sc->sstart, sc->smass);
+        const float gn = cc->lut[sg];
+        // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
+        pmf = 0.0;
+        {
+            const int k = tid, lane = tid & 31;
+            for (int q = 0; q < K; q++) {
+                const double mu = (double)mu_update2(rv.mu_b[q], rv.tb[q], rv.tc[q], rn, gn), inv = rv.inv_b[q];
+                const double cur = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k + 1], mu), inv), P.dist, pc);
+                double prev = __shfl_up_sync(0xffffffffu, cur, 1);
+                if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), inv), P.dist, pc);
+                const double d = __dsub_rn(cur, prev);
+                if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(rv.pi_b[q], d));
+            }
+        }
+        uint32_t bs, bm;
+        block_quantize(pmf, sc, bs, bm);
+        target = dec.target(r);
+        chain_symbol(sc, bs, bm, target);
+        if (P.trace_cdf) {
+            int32_t* row = P.trace_cdf + ((int64_t)img * N + n) * 3 * 257;
+            row[tid] = (int32_t)rs;
+            row[257 + tid] = (int32_t)gs;
+            row[514 + tid] = (int32_t)bs;
+            if (tid == 255) { row[256] = 65536; row[257 + 256] = 65536; row[514 + 256] = 65536; }
+        }
+        team_sync();
+        const int sb = sc->sym;
+        dec.advance(r, sc->sstart, sc->smass);
+        if (tid == 0) {
+            mbar_arrive(&cs->empty[s]);
+            const int32_t ij = __ldg(P.order + n);
+            uint8_t* px = im + ((int64_t)(ij >> 16) * P.W + (ij & 0xFFFF)) * 3;
+            px[0] = (uint8_t)sr; px[1] = (uint8_t)sg; px[2] = (uint8_t)sb;
+            st_release_u32(P.progress + img, (uint32_t)(n + 1));
+        }
+    }
+    if (tid == 0 && dec.status) atomicOr(P.status + img, dec.status);
+}
+
+template <int CP, int HH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DEC_THREADS, 1) k_decode2(DecParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int img = blockIdx.x >> 1;
+    if (cluster_rank() == 0) dec_consumer(P, img, smem);
+    else dec_producer<CP, HH>(P, img, smem);
+}
+
+}  // namespace lpic

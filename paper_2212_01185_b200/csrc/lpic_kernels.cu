@@ -5,8 +5,8 @@
 //                tables per pixel -> packed (start,width) in coding order
 //                (codec.py:116-183, kernels.py:88-114, 296-313)
 //   k_rc_encode  one range-coder lane (warp) per stream (coder.py:30-73)
-//   k_decode     persistent wavefront decoder, one CTA per stream
-//                (codec.py:193-247, coder.py:76-112)
+//   k_decode2    wavefront decoder, one 2-CTA cluster per stream
+//                (producer + serial chain, lpic_decode.cuh; codec.py:193-247)
 //   k_forward_taps / k_channel_cdfs / k_rc_decode_tables  parity seams
 #include "../../include/lpic_b200.h"
 
@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "lpic_cdf.cuh"
+#include "lpic_decode.cuh"
 #include "lpic_math.cuh"
 #include "lpic_net.cuh"
 #include "lpic_rc.cuh"
@@ -46,15 +47,6 @@ int fail(int code, const std::string& msg) {
 constexpr int NET_THREADS = 128;   // pixels per CTA tile (encoder) / per decoder chunk
 
 
-struct LdgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldg(p); } };
-struct LdcgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldcg(p); } };
-
-__device__ __forceinline__ void init_consts(float* lut, double* edges) {
-    for (int v = threadIdx.x; v < 256; v += blockDim.x)
-        lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);            // network.py:172-177
-    for (int k = threadIdx.x; k < 257; k += blockDim.x)
-        edges[k] = __ddiv_rn(2.0 * (double)k - 256.0, 255.0);            // kernels.py:34
-}
 
 template <int CP>
 __host__ __device__ constexpr size_t net_smem_bytes(int MP) {
@@ -78,13 +70,13 @@ k_encode(NetDev w, int K, int dist, const uint8_t* __restrict__ images, int H, i
          const int32_t* __restrict__ order, int64_t N, uint32_t* __restrict__ sw, int32_t* status,
          float* trace_raw, int32_t* trace_cdf) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* edges = reinterpret_cast<double*>(smem);                                   // 257
-    float* lut = reinterpret_cast<float*>(smem + 257 * 8 + 8);                          // 256
-    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + 257 * 8 + 8 + 1024);  // 4
-    float* raw = reinterpret_cast<float*>(smem + 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch));
+    CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
+    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
+    float* raw = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 4 * sizeof(WarpCdfScratch));
     float* zbuf = raw + NET_THREADS * w.MP;
+    const float* lut = cc->lut;
 
-    init_consts(lut, edges);
+    load_consts(cc);
     __syncthreads();
     const int img = blockIdx.y;
     const int tid = threadIdx.x;
@@ -117,7 +109,7 @@ k_encode(NetDev w, int K, int dist, const uint8_t* __restrict__ images, int H, i
 #pragma unroll 1
         for (int ch = 0; ch < 3; ch++) {
             uint32_t start[8], mass[8];
-            warp_table(raw + p * w.MP, K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, edges, sc + wid,
+            warp_table(raw + p * w.MP, K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, cc, sc + wid,
                        start, mass);
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
             if (lane == (sym >> 3)) {
@@ -158,89 +150,6 @@ k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, co
         lens[s] = len;
         if (e.status) atomicOr(status + s, e.status);
     }
-}
-
-// ---------------------------------------------------------------------------
-// wavefront decoder: one CTA per stream.  Per step: all pixels of the step
-// evaluate the network in parallel (their taps are decoded), then warp 0
-// runs the serial r -> g -> b chain (codec.py:218-246).
-// ---------------------------------------------------------------------------
-template <int CP, int HH>
-__global__ void __launch_bounds__(NET_THREADS)
-k_decode(NetDev w, int K, int dist, const uint8_t* __restrict__ payload, const int64_t* __restrict__ offs,
-         const int64_t* __restrict__ lens, int H, int W, int mode, uint8_t* images, int32_t* status,
-         float* trace_raw, int32_t* trace_cdf) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* edges = reinterpret_cast<double*>(smem);
-    float* lut = reinterpret_cast<float*>(smem + 257 * 8 + 8);
-    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + 257 * 8 + 8 + 1024);
-    float* raw = reinterpret_cast<float*>(smem + 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch));
-    float* zbuf = raw + NET_THREADS * w.MP;
-    __shared__ int s_stop;
-
-    init_consts(lut, edges);
-    if (threadIdx.x == 0) s_stop = 0;
-    __syncthreads();
-    const int img = blockIdx.x, tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-    const int64_t N = (int64_t)H * W;
-    uint8_t* im = images + (int64_t)img * N * 3;
-    const int a = sched_a(mode, W, HH);
-    const int64_t steps = sched_steps(mode, H, W, HH);
-    RcDecoder dec;
-    if (wid == 0) dec.init(payload + offs[img], lens[img]);
-    int64_t done = 0;
-    for (int64_t t = 0; t < steps; t++) {
-        int i_lo, i_hi;
-        sched_rows(t, a, H, W, i_lo, i_hi);
-        const int cnt = i_hi - i_lo + 1;
-        if (cnt <= 0) continue;
-        for (int c0 = 0; c0 < cnt; c0 += NET_THREADS) {
-            const int nb = min(NET_THREADS, cnt - c0);
-            if (tid < nb) {
-                const int i = i_lo + c0 + tid;
-                const int j = (int)(t - (int64_t)a * i);
-                float x[Taps<HH>::TC];
-                gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdcgU8());
-                net_forward<CP, Taps<HH>::TC>(w, x, raw + tid * w.MP, zbuf + tid, NET_THREADS);
-            }
-            __syncthreads();
-            if (wid == 0) {
-                for (int p = 0; p < nb; p++) {
-                    const int i = i_lo + c0 + p;
-                    const int j = (int)(t - (int64_t)a * i);
-                    const float* r = raw + p * w.MP;
-                    const int64_t n = done + c0 + p;
-                    if (trace_raw)
-                        for (int m = lane; m < w.M; m += 32) trace_raw[((int64_t)img * N + n) * w.M + m] = r[m];
-                    float rn = 0.0f, gn = 0.0f;
-                    int sym[3];
-#pragma unroll 1
-                    for (int ch = 0; ch < 3; ch++) {
-                        uint32_t start[8], mass[8];
-                        warp_table(r, K, dist, ch, rn, gn, edges, sc, start, mass);
-                        uint64_t rr;
-                        const uint32_t target = dec.target(rr);
-                        uint32_t s_st, s_ms;
-                        sym[ch] = warp_find_symbol(start, target, s_st, s_ms, mass);
-                        dec.advance(rr, s_st, s_ms);
-                        if (trace_cdf) store_cdf_row(trace_cdf + (((int64_t)img * N + n) * 3 + ch) * 257, start, mass);
-                        if (ch == 0) rn = lut[sym[0]];
-                        if (ch == 1) gn = lut[sym[1]];
-                    }
-                    if (lane == 0) {
-                        uint8_t* px = im + ((int64_t)i * W + j) * 3;
-                        px[0] = (uint8_t)sym[0]; px[1] = (uint8_t)sym[1]; px[2] = (uint8_t)sym[2];
-                    }
-                }
-                if (lane == 0 && dec.status) s_stop = 1;
-            }
-            __syncthreads();
-            if (s_stop) break;
-        }
-        if (s_stop) break;
-        done += cnt;
-    }
-    if (tid == 0 && dec.status) atomicOr(status + img, dec.status);
 }
 
 // ---------------------------------------------------------------------------
@@ -286,16 +195,15 @@ k_forward_full(NetDev w, const float* __restrict__ plane, int H, int W, float* _
 __global__ void __launch_bounds__(128)
 k_channel_cdfs(const float* __restrict__ raw, int64_t N, int M, int K, int dist, int ch,
                const float* __restrict__ rn, const float* __restrict__ gn, int32_t* __restrict__ out) {
-    __shared__ double edges[257];
-    __shared__ float lut[256];
+    __shared__ __align__(16) CdfConsts cc;
     __shared__ WarpCdfScratch sc[4];
-    init_consts(lut, edges);
+    load_consts(&cc);
     __syncthreads();
     const int wid = threadIdx.x >> 5;
     const int64_t n = (int64_t)blockIdx.x * 4 + wid;
     if (n >= N) return;
     uint32_t start[8], mass[8];
-    warp_table(raw + n * M, K, dist, ch, rn[n], gn[n], edges, sc + wid, start, mass);
+    warp_table(raw + n * M, K, dist, ch, rn[n], gn[n], &cc, sc + wid, start, mass);
     store_cdf_row(out + n * 257, start, mass);
 }
 
@@ -348,6 +256,15 @@ struct lpic_model {
     uint8_t* d_pack = nullptr; size_t pack_cap = 0;
     int64_t* d_meta = nullptr; size_t meta_cap = 0;   // lens | offs
     int32_t* d_status = nullptr; size_t status_cap = 0;
+    // decoder geometry tables (step offsets, producer chunks) per (H, W, mode)
+    int64_t* d_step_off = nullptr;
+    int32_t* d_chunks = nullptr;
+    int n_chunks = 0, ring_size = 0;
+    int dg_H = -1, dg_W = -1, dg_mode = -1;
+    // decoder ring workspace
+    uint8_t* d_ring = nullptr; size_t ring_cap = 0;
+    uint32_t* d_flags = nullptr; size_t flags_cap = 0;
+    uint32_t* d_progress = nullptr; size_t progress_cap = 0;
     int launches = 0;
     std::mutex mu;
 };
@@ -372,7 +289,7 @@ int set_smem(Kern k, size_t bytes) {
     return 0;
 }
 
-size_t table_smem() { return 257 * 8 + 8 + 1024 + 4 * sizeof(WarpCdfScratch); }
+size_t table_smem() { return sizeof(CdfConsts) + 4 * sizeof(WarpCdfScratch); }
 
 int coding_order(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
     if (m->d_order && m->ord_H == H && m->ord_W == W && m->ord_mode == mode) return 0;
@@ -420,14 +337,71 @@ template <int CP, int HH> struct EncodeRun {
     }
 };
 
+int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
+    if (m->d_step_off && m->dg_H == H && m->dg_W == W && m->dg_mode == mode) return 0;
+    const int a = sched_a(mode, W, m->h);
+    const int64_t steps = sched_steps(mode, H, W, m->h);
+    std::vector<int64_t> off((size_t)steps + 1);
+    std::vector<int32_t> chunks;
+    int64_t n = 0;
+    int maxc = 1;
+    for (int64_t t = 0; t < steps; t++) {
+        int lo, hi;
+        sched_rows(t, a, H, W, lo, hi);
+        off[(size_t)t] = n;
+        const int cnt = hi - lo + 1;
+        if (cnt <= 0) continue;
+        maxc = cnt > maxc ? cnt : maxc;
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+            chunks.push_back((int32_t)(n + c0));
+            chunks.push_back(cnt - c0 < 32 ? cnt - c0 : 32);
+        }
+        n += cnt;
+    }
+    off[(size_t)steps] = n;
+    int ring = 64;
+    while (ring < 2 * maxc + 64) ring <<= 1;
+    cudaFree(m->d_step_off); cudaFree(m->d_chunks);
+    m->d_step_off = nullptr; m->d_chunks = nullptr;
+    CUDA_TRY(cudaMalloc(&m->d_step_off, sizeof(int64_t) * off.size()));
+    CUDA_TRY(cudaMalloc(&m->d_chunks, sizeof(int32_t) * chunks.size()));
+    CUDA_TRY(cudaMemcpyAsync(m->d_step_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(m->d_chunks, chunks.data(), sizeof(int32_t) * chunks.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    m->n_chunks = (int)(chunks.size() / 2);
+    m->ring_size = ring;
+    m->dg_H = H; m->dg_W = W; m->dg_mode = mode;
+    return 0;
+}
+
+size_t dec_smem_bytes(int CP, int MP, int rec_bytes) {
+    const size_t prod = sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + (size_t)DEC_CHAIN_THREADS * MP * 4 +
+                        (size_t)DEC_CHAIN_THREADS * CP * 4;
+    const size_t cons = ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
+    return prod > cons ? prod : cons;
+}
+
 template <int CP, int HH> struct DecodeRun {
     static int run(lpic_model* m, const uint8_t* d_payload, const int64_t* d_offs, const int64_t* d_lens, int n,
                    int H, int W, int mode, uint8_t* d_images, int32_t* d_status, float* tr, int32_t* tc,
                    cudaStream_t st) {
-        const size_t smem = table_smem() + net_smem_bytes<CP>(m->MP);
-        if (set_smem(k_decode<CP, HH>, smem)) return LPIC_E_CUDA;
-        k_decode<CP, HH><<<n, NET_THREADS, smem, st>>>(m->net, m->K, m->dist, d_payload, d_offs, d_lens, H, W, mode,
-                                                        d_images, d_status, tr, tc);
+        if (int r = coding_order(m, H, W, mode, st)) return r;
+        if (int r = decode_geometry(m, H, W, mode, st)) return r;
+        const int rec = rec_bytes_for(m->K);
+        if (int r = ensure(m->d_ring, m->ring_cap, (size_t)n * m->ring_size * rec)) return r;
+        if (int r = ensure(m->d_flags, m->flags_cap, (size_t)n * m->ring_size)) return r;
+        if (int r = ensure(m->d_progress, m->progress_cap, (size_t)n)) return r;
+        CUDA_TRY(cudaMemsetAsync(m->d_flags, 0, sizeof(uint32_t) * n * m->ring_size, st));
+        CUDA_TRY(cudaMemsetAsync(m->d_progress, 0, sizeof(uint32_t) * n, st));
+        const size_t smem = dec_smem_bytes(CP, m->MP, rec);
+        if (set_smem(k_decode2<CP, HH>, smem)) return LPIC_E_CUDA;
+        DecParams P;
+        P.w = m->net; P.K = m->K; P.dist = m->dist; P.H = H; P.W = W; P.mode = mode; P.a = sched_a(mode, W, m->h);
+        P.N = (int64_t)H * W; P.payload = d_payload; P.offs = d_offs; P.lens = d_lens; P.images = d_images;
+        P.status = d_status; P.order = m->d_order; P.step_off = m->d_step_off; P.chunks = m->d_chunks;
+        P.n_chunks = m->n_chunks; P.ring = m->d_ring; P.flags = m->d_flags; P.progress = m->d_progress;
+        P.ring_size = m->ring_size; P.rec_bytes = rec; P.trace_raw = tr; P.trace_cdf = tc;
+        k_decode2<CP, HH><<<2 * n, DEC_THREADS, smem, st>>>(P);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -549,6 +523,8 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_w);
     cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_img); cudaFree(m->d_pay);
     cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
+    cudaFree(m->d_step_off); cudaFree(m->d_chunks); cudaFree(m->d_ring); cudaFree(m->d_flags);
+    cudaFree(m->d_progress);
     delete m;
     return 0;
 }

@@ -24,6 +24,11 @@ __host__ __device__ __forceinline__ void sched_rows(int64_t t, int a, int H, int
     i_hi = (int)(hi < H - 1 ? hi : H - 1);
 }
 
+// byte loaders for gather_u8: read-only path (encoder) / L2, bypassing L1
+// (decoder producer, which reads pixels another SM has just written)
+struct LdgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldg(p); } };
+struct LdcgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldcg(p); } };
+
 template <int HH> struct Taps {
     static constexpr int T = (2 * HH + 1) * HH + HH;
     static constexpr int TC = 3 * T;
