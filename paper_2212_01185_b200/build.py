@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "liblpic_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["lpic_kernels.cu"]
-HEADERS = ["lpic_math.cuh", "lpic_cdf.cuh", "lpic_rc.cuh", "lpic_net.cuh", "lpic_sched.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -27,9 +27,10 @@
 
 namespace lpic {
 
-constexpr int DEC_CHAIN_THREADS = 256;
-constexpr int DEC_THREADS = 288;        // + loader warp (consumer) / idle warp (producer)
+constexpr int DEC_CHAIN_THREADS = 256;   // == NT_THREADS: the producer runs net_tile
+constexpr int DEC_THREADS = 320;        // + loader and publisher warps (consumer) / idle in the producer
 constexpr int DEC_SLOTS = 4;
+constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publisher warp
 
 struct DecParams {
     NetDev w;
@@ -51,21 +52,30 @@ struct DecParams {
     int rec_bytes;
     float* trace_raw;
     int32_t* trace_cdf;
+    unsigned long long* dbg;     // optional timeline (globaltimer ns), see lpic_decode_debug
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // record layout
 __host__ __device__ __forceinline__ int rec_mix_off() { return 512; }
-__host__ __device__ __forceinline__ int rec_bytes_for(int K) { return (512 + 32 * K + 20 * K + 15) & ~15; }
+__host__ __device__ __forceinline__ int rec_bytes_for(int K) { return (512 + 32 * K + 20 * K + 4 + 15) & ~15; }
 struct RecView {
     const uint16_t* red;   // cdf[0..255]
     const double* pi_g; const double* inv_g; const double* pi_b; const double* inv_b;
     const float* mu_g; const float* mu_b; const float* ta; const float* tb; const float* tc;
+    int32_t ij;            // pixel (i<<16)|j
     __device__ RecView(const unsigned char* r, int K) {
         red = reinterpret_cast<const uint16_t*>(r);
         const double* d = reinterpret_cast<const double*>(r + 512);
         pi_g = d; inv_g = d + K; pi_b = d + 2 * K; inv_b = d + 3 * K;
         const float* f = reinterpret_cast<const float*>(d + 4 * K);
         mu_g = f; mu_b = f + K; ta = f + 2 * K; tb = f + 3 * K; tc = f + 4 * K;
+        ij = *reinterpret_cast<const int32_t*>(f + 5 * K);
     }
 };
 
@@ -74,6 +84,15 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Polling load: relaxed, L1-bypassing.  (ld.acquire.gpu compiles to
+// LDG.STRONG + CCTL.IVALL, i.e. it invalidates the whole L1 of the SM on
+// every poll; readers here only use L2 loads or TMA after the poll.)
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_smem(const volatile uint32_t* p) { return *p; }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -114,29 +133,37 @@ template <int CP, int HH>
 __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
     WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
-    float* raw = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch));
-    float* zbuf = raw + DEC_CHAIN_THREADS * P.w.MP;
+    float* fbase = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch));
+    constexpr int TC = Taps<HH>::TC;
+    NetTileBufs nb;
+    nb.act0 = fbase;
+    nb.act1 = nb.act0 + (CP > TC ? CP : TC) * NT_TP;
+    nb.wbuf = nb.act1 + CP * NT_TP;
+    nb.raw = nb.wbuf + ((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * P.w.MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
+                                                                           : CP * P.w.MT);
+    __shared__ long long s_need;
     load_consts(cc);
     __syncthreads();
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-    if (wid >= 8) return;
     const int K = P.K;
     const int64_t N = P.N;
     const uint8_t* im = P.images + (int64_t)img * N * 3;
     uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
     uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
     const uint32_t* progress = P.progress + img;
-    float* myraw = raw + tid * P.w.MP;
-    for (int c = wid; c < P.n_chunks; c += 8) {
+    for (int c = 0; c < P.n_chunks; c++) {
         const int n0 = P.chunks[2 * c], npx = P.chunks[2 * c + 1];
-        const int64_t n = n0 + lane;
-        const bool act = lane < npx;
+        const int64_t n = n0 + tid;
+        const bool act = tid < npx && tid < NT_TP;
         int i = 0, j = 0;
-        int64_t req = 0;
+        if (tid == 0) s_need = (int64_t)n0 + npx - P.ring_size;      // ring back-pressure
+        __syncthreads();
         if (act) {
+            // latest tap in coding order: (i, j-1) in step t-1, else all of step t-1
             const int32_t ij = __ldg(P.order + n);
             i = ij >> 16; j = ij & 0xFFFF;
             const int64_t t = (int64_t)P.a * i + j;
+            int64_t req;
             if (j >= 1) {
                 int lo, hi;
                 sched_rows(t - 1, P.a, P.H, P.W, lo, hi);
@@ -144,21 +171,29 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
             } else {
                 req = __ldg(P.step_off + t);
             }
+            atomicMax(&s_need, (long long)req);
         }
-        // also never run more than ring_size records ahead of the consumer
-        int64_t need = max(req, (int64_t)n0 + npx - P.ring_size);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
-        if (lane == 0) {
+        __syncthreads();
+        unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)c : nullptr;
+        if (tid == 0) {
+            if (dbg) dbg[0] = gtimer();
+            const int64_t need = s_need;
             uint32_t ns = 32;
-            while ((int64_t)ld_acquire_u32(progress) < need) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+            while ((int64_t)ld_relaxed_u32(progress) < need) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+            if (dbg) dbg[1] = gtimer();
         }
-        __syncwarp();
-        __threadfence();
+        __syncthreads();
         if (act) {
-            float x[Taps<HH>::TC];
+            float x[TC];
             gather_u8<HH>(im, P.H, P.W, i, j, P.mode, cc->lut, x, LdcgU8());
-            net_forward<CP, Taps<HH>::TC>(P.w, x, myraw, zbuf + tid, DEC_CHAIN_THREADS);
+#pragma unroll
+            for (int q = 0; q < TC; q++) nb.act0[q * NT_TP + tid] = x[q];
+        }
+        __syncthreads();
+        net_tile<CP, TC>(P.w, nb);
+        if (dbg && tid == 0) dbg[2] = gtimer();
+        if (act) {
+            const float* myraw = nb.raw + tid * P.w.MP;
             if (P.trace_raw)
                 for (int m = 0; m < P.w.M; m++) P.trace_raw[((int64_t)img * N + n) * P.w.M + m] = myraw[m];
             // g/b mixture record (kernels.py:212-247 minus the rn/gn-dependent update)
@@ -176,22 +211,22 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
                 f[3 * K + q] = tanhf_glibc(myraw[10 * K + q]);
                 f[4 * K + q] = tanhf_glibc(myraw[11 * K + q]);
             }
+            *reinterpret_cast<int32_t*>(f + 5 * K) = (i << 16) | j;
         }
-        __syncwarp();
-        // red tables, one warp-built table per pixel of the chunk
-        for (int p = 0; p < npx; p++) {
+        // red tables: warp w builds the tables of pixels w, w+8, ...
+        for (int p = wid; wid < 8 && p < npx; p += 8) {
             uint32_t start[8], mass[8];
-            warp_table(raw + (wid * 32 + p) * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
-            const int64_t np = n0 + p;
-            unsigned char* rec = ring + (int64_t)(np & (P.ring_size - 1)) * P.rec_bytes;
+            warp_table(nb.raw + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
+            unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
             uint4 v;
             v.x = (start[0] & 0xFFFFu) | (start[1] << 16); v.y = (start[2] & 0xFFFFu) | (start[3] << 16);
             v.z = (start[4] & 0xFFFFu) | (start[5] << 16); v.w = (start[6] & 0xFFFFu) | (start[7] << 16);
             reinterpret_cast<uint4*>(rec)[lane] = v;
         }
         __threadfence();
-        __syncwarp();
+        __syncthreads();
         if (act) st_release_u32(flags + (n & (P.ring_size - 1)), (uint32_t)(n + 1));
+        if (dbg && tid == 0) dbg[3] = gtimer();
     }
 }
 
@@ -201,8 +236,57 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
 struct ConsumerSmem {
     uint64_t full[DEC_SLOTS];
     uint64_t empty[DEC_SLOTS];
+    uint32_t pubq[DEC_PUBQ][2];  // (i<<16|j, r|g<<8|b<<16) for the publisher
+    uint32_t chain_done, pub_done;
+    double wedge[8][4];          // per-warp last upper-edge CDF values (chain_pmf)
     BlockCdfScratch sc;
 };
+
+// Per-bin PMF of one chain table (thread k = bin k).  The K <= 4 components
+// are evaluated branch-free in one batch so their Phi latencies overlap; the
+// lower edge of a warp's first bin is the upper edge of the previous warp's
+// last bin, passed through shared memory (one team barrier instead of a
+// divergent extra evaluation).
+constexpr int CHAIN_KU = 4;
+template <bool BLUE>
+__device__ __forceinline__ double chain_pmf(const double* pi, const double* inv, const float* mu0, const float* t1,
+                                           const float* t2, float rn, float gn, int K, int dist, const CdfConsts* cc,
+                                           double (*wedge)[CHAIN_KU]) {
+    const int k = threadIdx.x, lane = k & 31, wid = k >> 5;
+    double cur[CHAIN_KU];
+    const double e_hi = cc->edges[k + 1];
+#pragma unroll
+    for (int q = 0; q < CHAIN_KU; q++) {
+        const int qq = q < K ? q : 0;                     // padded components: evaluated, then ignored
+        const float m32 = BLUE ? mu_update2(mu0[qq], t1[qq], t2[qq], rn, gn) : mu_update1(mu0[qq], t1[qq], rn);
+        const double c = cdf_value(__dmul_rn(__dsub_rn(e_hi, (double)m32), inv[qq]), dist, cc->phic);
+        cur[q] = (k == 255) ? 1.0 : c;
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int q = 0; q < CHAIN_KU; q++) wedge[wid][q] = cur[q];
+    }
+    team_sync();
+    double pmf = 0.0;
+#pragma unroll
+    for (int q = 0; q < CHAIN_KU; q++) {
+        double prev = __shfl_up_sync(0xffffffffu, cur[q], 1);
+        if (lane == 0) prev = (wid == 0) ? 0.0 : wedge[wid - 1][q];
+        const double d = __dsub_rn(cur[q], prev);
+        const double np = __dadd_rn(pmf, __dmul_rn(pi[q < K ? q : 0], d));
+        pmf = (q < K && d > 0.0) ? np : pmf;
+    }
+    for (int q = CHAIN_KU; q < K; q++) {                  // K > 4: plain loop
+        const float m32 = BLUE ? mu_update2(mu0[q], t1[q], t2[q], rn, gn) : mu_update1(mu0[q], t1[q], rn);
+        const double mu = (double)m32, iv = inv[q];
+        const double c = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(e_hi, mu), iv), dist, cc->phic);
+        double prev = __shfl_up_sync(0xffffffffu, c, 1);
+        if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), iv), dist, cc->phic);
+        const double d = __dsub_rn(c, prev);
+        if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(pi[q], d));
+    }
+    return pmf;
+}
 
 __device__ __forceinline__ void chain_symbol(BlockCdfScratch* sc, uint32_t start, uint32_t mass, uint32_t target) {
     if (start <= target && target < start + mass) { sc->sym = threadIdx.x; sc->sstart = start; sc->smass = mass; }
@@ -216,6 +300,7 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
     const int tid = threadIdx.x, wid = tid >> 5;
     if (tid == 0) {
         for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&cs->full[s], 1); mbar_init(&cs->empty[s], 1); }
+        cs->chain_done = 0; cs->pub_done = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -230,7 +315,7 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
                 if (n >= DEC_SLOTS) mbar_wait(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1));
                 const uint32_t* fl = flags + (n & (P.ring_size - 1));
                 uint32_t ns = 32;
-                while (ld_acquire_u32(fl) != (uint32_t)(n + 1)) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+                while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 mbar_arrive_tx(&cs->full[s], (uint32_t)P.rec_bytes);
                 bulk_g2s(slots + s * P.rec_bytes, ring + (int64_t)(n & (P.ring_size - 1)) * P.rec_bytes,
@@ -240,13 +325,35 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         return;
     }
     uint8_t* im = P.images + (int64_t)img * N * 3;
+    if (wid == 9) {                                   // publisher warp: pixels -> global, progress
+        if ((tid & 31) == 0) {
+            volatile uint32_t* done = &cs->chain_done;
+            int64_t pub = 0;
+            while (pub < N) {
+                uint32_t avail = *done;
+                if ((int64_t)avail <= pub) { __nanosleep(20); continue; }
+                for (; pub < (int64_t)avail; pub++) {
+                    const volatile uint32_t* q = cs->pubq[pub % DEC_PUBQ];
+                    const uint32_t ij = q[0], rgb = q[1];
+                    uint8_t* px = im + ((int64_t)(ij >> 16) * P.W + (ij & 0xFFFF)) * 3;
+                    px[0] = (uint8_t)rgb; px[1] = (uint8_t)(rgb >> 8); px[2] = (uint8_t)(rgb >> 16);
+                }
+                *(volatile uint32_t*)&cs->pub_done = (uint32_t)pub;
+                st_release_u32(P.progress + img, (uint32_t)pub);
+            }
+        }
+        return;
+    }
     RcDecoder dec;
     dec.init(P.payload + P.offs[img], P.lens[img]);
     BlockCdfScratch* sc = &cs->sc;
     const double* pc = cc->phic;
     for (int64_t n = 0; n < N; n++) {
         const int s = (int)(n % DEC_SLOTS);
+        unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)P.n_chunks + 12 * n : nullptr;
+        if (dbg && tid == 0) dbg[0] = gtimer();
         mbar_wait(&cs->full[s], (uint32_t)((n / DEC_SLOTS) & 1));
+        if (dbg && tid == 0) { dbg[1] = gtimer(); dbg[3] = clock64(); }
         const RecView rv(slots + s * P.rec_bytes, K);
         // ---- red: table precomputed by the producer
         uint64_t r;
@@ -258,21 +365,13 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         const int sr = sc->sym;
         dec.advance(r, sc->sstart, sc->smass);
         const float rn = cc->lut[sr];
+        if (dbg && tid == 0) dbg[4] = clock64();
         // ---- green: mu_g += tanh(alpha)*rn (kernels.py:236-237)
-        double pmf = 0.0;
-        {
-            const int k = tid, lane = tid & 31;
-            for (int q = 0; q < K; q++) {
-                const double mu = (double)mu_update1(rv.mu_g[q], rv.ta[q], rn), inv = rv.inv_g[q];
-                const double cur = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k + 1], mu), inv), P.dist, pc);
-                double prev = __shfl_up_sync(0xffffffffu, cur, 1);
-                if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), inv), P.dist, pc);
-                const double d = __dsub_rn(cur, prev);
-                if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(rv.pi_g[q], d));
-            }
-        }
+        double pmf = chain_pmf<false>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, cs->wedge);
+        if (dbg && tid == 0) dbg[5] = clock64();
         uint32_t gs, gm;
         block_quantize(pmf, sc, gs, gm);
+        if (dbg && tid == 0) dbg[6] = clock64();
         target = dec.target(r);
         chain_symbol(sc, gs, gm, target);
         team_sync();
@@ -280,20 +379,11 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         dec.advance(r, sc->sstart, sc->smass);
         const float gn = cc->lut[sg];
         // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
-        pmf = 0.0;
-        {
-            const int k = tid, lane = tid & 31;
-            for (int q = 0; q < K; q++) {
-                const double mu = (double)mu_update2(rv.mu_b[q], rv.tb[q], rv.tc[q], rn, gn), inv = rv.inv_b[q];
-                const double cur = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k + 1], mu), inv), P.dist, pc);
-                double prev = __shfl_up_sync(0xffffffffu, cur, 1);
-                if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), inv), P.dist, pc);
-                const double d = __dsub_rn(cur, prev);
-                if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(rv.pi_b[q], d));
-            }
-        }
+        pmf = chain_pmf<true>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, cs->wedge);
+        if (dbg && tid == 0) dbg[7] = clock64();
         uint32_t bs, bm;
         block_quantize(pmf, sc, bs, bm);
+        if (dbg && tid == 0) dbg[8] = clock64();
         target = dec.target(r);
         chain_symbol(sc, bs, bm, target);
         if (P.trace_cdf) {
@@ -308,10 +398,12 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         dec.advance(r, sc->sstart, sc->smass);
         if (tid == 0) {
             mbar_arrive(&cs->empty[s]);
-            const int32_t ij = __ldg(P.order + n);
-            uint8_t* px = im + ((int64_t)(ij >> 16) * P.W + (ij & 0xFFFF)) * 3;
-            px[0] = (uint8_t)sr; px[1] = (uint8_t)sg; px[2] = (uint8_t)sb;
-            st_release_u32(P.progress + img, (uint32_t)(n + 1));
+            while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ <= n) __nanosleep(20);
+            cs->pubq[n % DEC_PUBQ][0] = (uint32_t)rv.ij;
+            cs->pubq[n % DEC_PUBQ][1] = (uint32_t)sr | ((uint32_t)sg << 8) | ((uint32_t)sb << 16);
+            __threadfence_block();
+            *(volatile uint32_t*)&cs->chain_done = (uint32_t)(n + 1);
+            if (dbg) { dbg[2] = gtimer(); dbg[9] = clock64(); }
         }
     }
     if (tid == 0 && dec.status) atomicOr(P.status + img, dec.status);

@@ -62,64 +62,92 @@ __device__ __forceinline__ void store_cdf_row(int32_t* row, const uint32_t start
 }
 
 // ---------------------------------------------------------------------------
-// encoder: network + tables for 128 pixels (coding order) per CTA
+// encoder, stage 1: the network over 64-pixel tiles in coding order
+// (codec.py:116-145 + kernels.py:88-114): gather -> net_tile -> raw plane
 // ---------------------------------------------------------------------------
 template <int CP, int HH>
-__global__ void __launch_bounds__(NET_THREADS)
-k_encode(NetDev w, int K, int dist, const uint8_t* __restrict__ images, int H, int W, int mode,
-         const int32_t* __restrict__ order, int64_t N, uint32_t* __restrict__ sw, int32_t* status,
-         float* trace_raw, int32_t* trace_cdf) {
+__global__ void __launch_bounds__(NT_THREADS)
+k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, const int32_t* __restrict__ order,
+          int64_t N, float* __restrict__ raw_out, int32_t* status, float* trace_raw) {
     extern __shared__ __align__(16) unsigned char smem[];
-    CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
-    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
-    float* raw = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 4 * sizeof(WarpCdfScratch));
-    float* zbuf = raw + NET_THREADS * w.MP;
-    const float* lut = cc->lut;
-
-    load_consts(cc);
+    constexpr int TC = Taps<HH>::TC;
+    __shared__ float lut[256];
+    float* fb = reinterpret_cast<float*>(smem);
+    NetTileBufs nb;
+    nb.act0 = fb;
+    nb.act1 = nb.act0 + (CP > TC ? CP : TC) * NT_TP;
+    nb.wbuf = nb.act1 + CP * NT_TP;
+    nb.raw = nb.wbuf + ((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * w.MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
+                                                                         : CP * w.MT);
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
     __syncthreads();
-    const int img = blockIdx.y;
-    const int tid = threadIdx.x;
-    const int64_t n0 = (int64_t)blockIdx.x * NET_THREADS;
+    const int img = blockIdx.y, tid = threadIdx.x;
+    const int64_t n0 = (int64_t)blockIdx.x * NT_TP;
     const uint8_t* im = images + (int64_t)img * N * 3;
-    const int64_t n = n0 + tid;
-    if (n < N) {
-        const int32_t ij = __ldg(order + n);
-        const int i = ij >> 16, j = ij & 0xFFFF;
-        float x[Taps<HH>::TC];
-        gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdgU8());
-        float* r = raw + tid * w.MP;
-        net_forward<CP, Taps<HH>::TC>(w, x, r, zbuf + tid, NET_THREADS);
-        bool finite = true;
-        for (int m = 0; m < w.M; m++) finite &= isfinite(r[m]);
-        if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
-        if (trace_raw)
-            for (int m = 0; m < w.M; m++) trace_raw[((int64_t)img * N + n) * w.M + m] = r[m];
+    if (tid < NT_TP) {
+        float x[TC];
+        const int64_t n = n0 + tid;
+        if (n < N) {
+            const int32_t ij = __ldg(order + n);
+            gather_u8<HH>(im, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+        } else {
+#pragma unroll
+            for (int q = 0; q < TC; q++) x[q] = 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < TC; q++) nb.act0[q * NT_TP + tid] = x[q];
     }
     __syncthreads();
-    const int wid = tid >> 5, lane = tid & 31;
-    const int cnt = (int)((N - n0) < NET_THREADS ? (N - n0) : NET_THREADS);
-    for (int p = wid * 32; p < min(cnt, wid * 32 + 32); p++) {
-        const int64_t nn = n0 + p;
+    net_tile<CP, TC>(w, nb);
+    const int np = (int)((N - n0) < NT_TP ? (N - n0) : NT_TP);
+    bool finite = true;
+    for (int e = tid; e < np * w.M; e += NT_THREADS) {
+        const int p = e / w.M, m = e - p * w.M;
+        const float v = nb.raw[p * w.MP + m];
+        finite &= isfinite(v);
+        raw_out[((int64_t)img * N + n0 + p) * w.M + m] = v;
+        if (trace_raw) trace_raw[((int64_t)img * N + n0 + p) * w.M + m] = v;
+    }
+    if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
+// encoder, stage 2: three quantised CDF tables per pixel (warp builder) and
+// the coded symbol's (start, width) in coding order (codec.py:168-182)
+// ---------------------------------------------------------------------------
+constexpr int TAB_WARPS = 8;
+__global__ void __launch_bounds__(TAB_WARPS * 32)
+k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
+             const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
+             int32_t* trace_cdf) {
+    __shared__ __align__(16) CdfConsts cc;
+    __shared__ WarpCdfScratch sc[TAB_WARPS];
+    __shared__ float rbuf[TAB_WARPS][12 * KMAX];
+    load_consts(&cc);
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t g = (int64_t)blockIdx.x * TAB_WARPS + wid; g < total; g += (int64_t)gridDim.x * TAB_WARPS) {
+        const int64_t img = g / N, nn = g - img * N;
+        for (int m = lane; m < M; m += 32) rbuf[wid][m] = __ldg(raw + g * M + m);
         const int32_t ij = __ldg(order + nn);
-        const int i = ij >> 16, j = ij & 0xFFFF;
-        const uint8_t* px = im + ((int64_t)i * W + j) * 3;
+        const uint8_t* px = images + ((int64_t)img * N + (int64_t)(ij >> 16) * W + (ij & 0xFFFF)) * 3;
         const int s0 = __ldg(px), s1 = __ldg(px + 1), s2 = __ldg(px + 2);
-        const float rn = lut[s0], gn = lut[s1];
+        const float rn = cc.lut[s0], gn = cc.lut[s1];
+        __syncwarp();
 #pragma unroll 1
         for (int ch = 0; ch < 3; ch++) {
             uint32_t start[8], mass[8];
-            warp_table(raw + p * w.MP, K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, cc, sc + wid,
-                       start, mass);
+            warp_table(rbuf[wid], K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, sc + wid, start, mass);
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
             if (lane == (sym >> 3)) {
                 uint32_t st = 0, ms = 1;
 #pragma unroll
                 for (int q = 0; q < 8; q++) if (q == (sym & 7)) { st = start[q]; ms = mass[q]; }
-                sw[((int64_t)img * N + nn) * 3 + ch] = (st << 16) | (ms - 1);
+                sw[g * 3 + ch] = (st << 16) | (ms - 1);
             }
-            if (trace_cdf) store_cdf_row(trace_cdf + (((int64_t)img * N + nn) * 3 + ch) * 257, start, mass);
+            if (trace_cdf) store_cdf_row(trace_cdf + (g * 3 + ch) * 257, start, mass);
         }
+        __syncwarp();
     }
 }
 
@@ -240,7 +268,7 @@ __global__ void k_pack(const uint8_t* src, int64_t cap_each, const int64_t* offs
 // host side: the model handle and the C-ABI
 // ===========================================================================
 struct lpic_model {
-    int K, C, L, h, dist, M, T, TC, CP, MP, NH;
+    int K, C, L, h, dist, M, T, TC, CP, MP, MT, NH;
     int device;
     int precision;
     uint64_t fingerprint;
@@ -251,6 +279,7 @@ struct lpic_model {
     int ord_H = -1, ord_W = -1, ord_mode = -1;
     // workspace
     uint32_t* d_sw = nullptr; size_t sw_cap = 0;
+    float* d_raw = nullptr; size_t raw_cap = 0;
     uint8_t* d_img = nullptr; size_t img_cap = 0;
     uint8_t* d_pay = nullptr; size_t pay_cap = 0;
     uint8_t* d_pack = nullptr; size_t pack_cap = 0;
@@ -265,6 +294,7 @@ struct lpic_model {
     uint8_t* d_ring = nullptr; size_t ring_cap = 0;
     uint32_t* d_flags = nullptr; size_t flags_cap = 0;
     uint32_t* d_progress = nullptr; size_t progress_cap = 0;
+    unsigned long long* d_dbg = nullptr;   // optional decoder timeline (lpic_decode_debug)
     int launches = 0;
     std::mutex mu;
 };
@@ -324,14 +354,21 @@ int dispatch(int CP, int HH, A&&... args) {
 }
 
 template <int CP, int HH> struct EncodeRun {
-    static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, uint32_t* sw,
+    static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw, uint32_t* sw,
                    int32_t* d_status, float* tr, int32_t* tc, cudaStream_t st) {
-        const size_t smem = table_smem() + net_smem_bytes<CP>(m->MP);
-        if (set_smem(k_encode<CP, HH>, smem)) return LPIC_E_CUDA;
+        constexpr int TC = Taps<HH>::TC;
+        const size_t smem = net_tile_floats(CP, TC, m->MT, m->MP) * 4;
+        if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
         const int64_t N = (int64_t)H * W;
-        dim3 grid((unsigned)((N + NET_THREADS - 1) / NET_THREADS), (unsigned)n);
-        k_encode<CP, HH><<<grid, NET_THREADS, smem, st>>>(m->net, m->K, m->dist, d_images, H, W, mode, m->d_order,
-                                                           N, sw, d_status, tr, tc);
+        dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
+        k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status, tr);
+        CUDA_TRY(cudaGetLastError());
+        const int64_t total = N * n;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+        const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
+        const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
+        k_enc_tables<<<g2, TAB_WARPS * 32, 0, st>>>(raw, m->M, m->K, m->dist, d_images, W, m->d_order, N, total, sw, tc);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -352,9 +389,9 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
         const int cnt = hi - lo + 1;
         if (cnt <= 0) continue;
         maxc = cnt > maxc ? cnt : maxc;
-        for (int c0 = 0; c0 < cnt; c0 += 32) {
+        for (int c0 = 0; c0 < cnt; c0 += NT_TP) {
             chunks.push_back((int32_t)(n + c0));
-            chunks.push_back(cnt - c0 < 32 ? cnt - c0 : 32);
+            chunks.push_back(cnt - c0 < NT_TP ? cnt - c0 : NT_TP);
         }
         n += cnt;
     }
@@ -374,9 +411,8 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
     return 0;
 }
 
-size_t dec_smem_bytes(int CP, int MP, int rec_bytes) {
-    const size_t prod = sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + (size_t)DEC_CHAIN_THREADS * MP * 4 +
-                        (size_t)DEC_CHAIN_THREADS * CP * 4;
+size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes) {
+    const size_t prod = sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + net_tile_floats(CP, TC, MT, MP) * 4;
     const size_t cons = ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
     return prod > cons ? prod : cons;
 }
@@ -393,7 +429,7 @@ template <int CP, int HH> struct DecodeRun {
         if (int r = ensure(m->d_progress, m->progress_cap, (size_t)n)) return r;
         CUDA_TRY(cudaMemsetAsync(m->d_flags, 0, sizeof(uint32_t) * n * m->ring_size, st));
         CUDA_TRY(cudaMemsetAsync(m->d_progress, 0, sizeof(uint32_t) * n, st));
-        const size_t smem = dec_smem_bytes(CP, m->MP, rec);
+        const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec);
         if (set_smem(k_decode2<CP, HH>, smem)) return LPIC_E_CUDA;
         DecParams P;
         P.w = m->net; P.K = m->K; P.dist = m->dist; P.H = H; P.W = W; P.mode = mode; P.a = sched_a(mode, W, m->h);
@@ -401,6 +437,7 @@ template <int CP, int HH> struct DecodeRun {
         P.status = d_status; P.order = m->d_order; P.step_off = m->d_step_off; P.chunks = m->d_chunks;
         P.n_chunks = m->n_chunks; P.ring = m->d_ring; P.flags = m->d_flags; P.progress = m->d_progress;
         P.ring_size = m->ring_size; P.rec_bytes = rec; P.trace_raw = tr; P.trace_cdf = tc;
+        P.dbg = m->d_dbg;
         k_decode2<CP, HH><<<2 * n, DEC_THREADS, smem, st>>>(P);
         CUDA_TRY(cudaGetLastError());
         return 0;
@@ -466,38 +503,51 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
     m->M = 12 * K; m->T = (2 * h + 1) * h + h; m->TC = 3 * m->T;
     m->CP = C <= 16 ? 16 : C <= 32 ? 32 : C <= 64 ? 64 : 128;
     m->MP = (m->M + 3) & ~3;
+    m->MT = (m->M + 15) & ~15;
     m->NH = L - 2;
     m->precision = LPIC_PREC_COMPAT;
     cudaGetDevice(&m->device);
-    const int CP = m->CP, MP = m->MP, NH = m->NH, T = m->T, TC = m->TC, M = m->M;
+    const int CP = m->CP, MP = m->MP, MT = m->MT, NH = m->NH, T = m->T, TC = m->TC, M = m->M;
     // padded host layouts
     std::vector<float> mwT((size_t)CP * TC, 0.f), mb(CP, 0.f), hw((size_t)NH * CP * CP, 0.f), hb((size_t)NH * CP, 0.f),
-        ow((size_t)MP * CP, 0.f), ob(MP, 0.f);
+        ow((size_t)MP * CP, 0.f), ob(MT, 0.f), mwI((size_t)TC * CP, 0.f), hwI((size_t)NH * CP * CP, 0.f),
+        owI((size_t)CP * MT, 0.f);
     for (int t = 0; t < T; t++)
         for (int c = 0; c < 3; c++)
-            for (int f = 0; f < C; f++) mwT[(size_t)f * TC + t * 3 + c] = masked_w[(t * 3 + c) * C + f];
+            for (int f = 0; f < C; f++) {
+                mwT[(size_t)f * TC + t * 3 + c] = masked_w[(t * 3 + c) * C + f];
+                mwI[(size_t)(t * 3 + c) * CP + f] = masked_w[(t * 3 + c) * C + f];
+            }
     for (int f = 0; f < C; f++) mb[f] = masked_b[f];
     for (int l = 0; l < NH; l++)
         for (int o = 0; o < C; o++) {
-            for (int i = 0; i < C; i++) hw[((size_t)l * CP + o) * CP + i] = hidden_w[((size_t)l * C + o) * C + i];
+            for (int i = 0; i < C; i++) {
+                hw[((size_t)l * CP + o) * CP + i] = hidden_w[((size_t)l * C + o) * C + i];
+                hwI[((size_t)l * CP + i) * CP + o] = hidden_w[((size_t)l * C + o) * C + i];
+            }
             hb[(size_t)l * CP + o] = hidden_b[(size_t)l * C + o];
         }
     for (int mm = 0; mm < M; mm++) {
-        for (int i = 0; i < C; i++) ow[(size_t)mm * CP + i] = out_w[(size_t)mm * C + i];
+        for (int i = 0; i < C; i++) {
+            ow[(size_t)mm * CP + i] = out_w[(size_t)mm * C + i];
+            owI[(size_t)i * MT + mm] = out_w[(size_t)mm * C + i];
+        }
         ob[mm] = out_b[mm];
     }
-    const size_t total = mwT.size() + mb.size() + hw.size() + hb.size() + ow.size() + ob.size();
+    const size_t total = mwT.size() + mb.size() + hw.size() + hb.size() + ow.size() + ob.size() + mwI.size() +
+                         hwI.size() + owI.size() + 64;
     if (cudaMalloc(&m->d_w, total * sizeof(float)) != cudaSuccess) { delete m; return fail(LPIC_E_NOMEM, "cudaMalloc weights"); }
     float* p = m->d_w;
     auto put = [&](const std::vector<float>& v) -> const float* {
         cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice);
         const float* r = p;
-        p += v.size();
+        p += (v.size() + 3) & ~(size_t)3;                 // keep every tensor 16-byte aligned
         return r;
     };
     m->net.mwT = put(mwT); m->net.mb = put(mb); m->net.hw = put(hw); m->net.hb = put(hb);
-    m->net.ow = put(ow); m->net.ob = put(ob);
+    m->net.ow = put(ow); m->net.ob = put(ob); m->net.mwI = put(mwI); m->net.hwI = put(hwI); m->net.owI = put(owI);
     m->net.C = C; m->net.CP = CP; m->net.M = M; m->net.MP = MP; m->net.NH = NH; m->net.T = T; m->net.TC = TC;
+    m->net.MT = MT;
     // fingerprint of the LPWT serialisation (network.py:255-281)
     std::vector<uint8_t> ser;
     const char magic[4] = {'L', 'P', 'W', 'T'};
@@ -521,7 +571,7 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
 int lpic_model_destroy(lpic_model_t* m) {
     if (!m) return 0;
     cudaFree(m->d_w);
-    cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_img); cudaFree(m->d_pay);
+    cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_raw); cudaFree(m->d_img); cudaFree(m->d_pay);
     cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
     cudaFree(m->d_step_off); cudaFree(m->d_chunks); cudaFree(m->d_ring); cudaFree(m->d_flags);
     cudaFree(m->d_progress);
@@ -538,6 +588,16 @@ int lpic_model_set_precision(lpic_model_t* m, int precision) {
 
 uint64_t lpic_model_fingerprint(const lpic_model_t* m) { return m ? m->fingerprint : 0; }
 int lpic_last_launch_count(const lpic_model_t* m) { return m ? m->launches : 0; }
+
+/* Diagnostics (not part of include/lpic_b200.h): record a globaltimer
+ * timeline of stream 0 of the next decode into d_buf (4 stamps per producer
+ * chunk followed by 3 per pixel); pass NULL to disable.  Returns the number
+ * of producer chunks of the last decode geometry. */
+int lpic_decode_debug(lpic_model_t* m, unsigned long long* d_buf) {
+    if (!m) return -1;
+    m->d_dbg = d_buf;
+    return m->n_chunks;
+}
 
 int lpic_forward_taps(lpic_model_t* m, const float* d_taps, int64_t N, float* d_raw, void* stream) {
     if (!m || N < 0) return fail(LPIC_E_ARG, "bad argument");
@@ -587,13 +647,14 @@ int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, in
     const int64_t N = (int64_t)H * W;
     if (int r = coding_order(m, H, W, mode, st)) return r;
     if (int r = ensure(m->d_sw, m->sw_cap, (size_t)n * N * 3)) return r;
+    if (int r = ensure(m->d_raw, m->raw_cap, (size_t)n * N * m->M)) return r;
     CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
-    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_sw, d_status, d_trace_raw,
-                                    d_trace_cdf, st))
+    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
+                                    d_trace_raw, d_trace_cdf, st))
         return r;
     k_rc_encode<<<n, 32, 0, st>>>(m->d_sw, nullptr, nullptr, 3 * N, d_payload, cap_each, d_lens, d_status);
     CUDA_TRY(cudaGetLastError());
-    m->launches = 2;
+    m->launches = 3;
     return 0;
 }
 

@@ -90,11 +90,17 @@ struct RcDecoder {
         data = d; len = n; pos = 0; virt = 0; status = ST_OK; range = RC_TOP - 1; code = 0;
         for (int k = 0; k < 6; k++) code = (code << 8) | (uint64_t)next_byte();
     }
-    // target = min(code // r, 65535) (coder.py:100-103), exact via a float64
-    // quotient (code < 2^48, r < 2^32) and one integer correction.
+    // target = min(code // r, 65535) (coder.py:100-103), exact: a float64
+    // quotient estimate (code < 2^48, 2^24 <= r < 2^32, so q < 2^24 and the
+    // refined reciprocal is off by far less than one unit) plus one integer
+    // correction each way.
     __device__ __forceinline__ uint32_t target(uint64_t& r_out) const {
         const uint64_t r = range >> 16;
-        uint64_t q = (uint64_t)__ddiv_rz((double)code, (double)r);
+        const double rd = (double)r;
+        double y;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(rd));
+        y = __fma_rn(y, __fma_rn(-rd, y, 1.0), y);
+        uint64_t q = (uint64_t)__dmul_rz((double)code, y);
         if (q * r > code) q--;
         else if ((q + 1) * r <= code) q++;
         r_out = r;

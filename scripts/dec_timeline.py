@@ -1,0 +1,44 @@
+"""Decoder timeline: producer chunk / consumer pixel timestamps for stream 0."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2212_01185_b200 as P
+from paper_2212_01185_b200 import _native, synth
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+W = int(sys.argv[2]) if len(sys.argv) > 2 else H
+w, cfg = synth.baseline_weights()
+imgs = synth.batch(1, H, W)
+cs = P.encode_batch(imgs, w, cfg, "wave")
+m = P.network.gpu_model(w, cfg)
+L = _native.load()
+L.lpic_decode_debug.argtypes = [C.c_void_p, C.c_void_p]
+P.decode_batch(cs, w, cfg)                          # builds the geometry tables
+nch = L.lpic_decode_debug(m.handle, None)
+N = H * W
+buf = torch.zeros(4 * nch + 12 * N, dtype=torch.int64, device="cuda")
+L.lpic_decode_debug(m.handle, buf.data_ptr())
+out = P.decode_batch(cs, w, cfg)
+L.lpic_decode_debug(m.handle, None)
+assert np.array_equal(out[0], imgs[0])
+b = buf.cpu().numpy().astype(np.float64)
+t0 = min(b[:4 * nch][b[:4 * nch] > 0].min(), b[4 * nch:].reshape(-1, 12)[:, 0].min())
+pc = (b[:4 * nch].reshape(nch, 4) - t0) / 1e3     # us
+raw12 = b[4 * nch:].reshape(N, 12)
+cp = (raw12[:, :3] - t0) / 1e3
+clk = raw12[:, 3:10]
+print(f"total {cp[-1, 2]:.1f} us for {N} px ({cp[-1,2]/N:.2f} us/px), {nch} chunks")
+print("producer: wait %.1f us/chunk, net+mix %.1f, tables %.1f (means)" % (
+    np.mean(pc[:, 1] - pc[:, 0]), np.mean(pc[:, 2] - pc[:, 1]), np.mean(pc[:, 3] - pc[:, 2])))
+print("consumer: full-wait %.2f us/px, chain %.2f us/px" % (np.mean(cp[:, 1] - cp[:, 0]), np.mean(cp[:, 2] - cp[:, 1])))
+np.save("gpurun_out/timeline.npy", b)
+mid = clk[N // 4: 3 * N // 4]
+print("chain phases (cycles/px): red-search %.0f green-pmf %.0f green-quant %.0f green-dec+blue-pmf %.0f blue-quant %.0f "
+      "blue-dec+write %.0f" % tuple(np.mean(np.diff(mid, axis=1), axis=0)))
+print("chain total cycles/px %.0f" % np.mean(mid[:, -1] - mid[:, 0]))
+for k in list(range(0, min(nch, 12))) + list(range(nch // 2, nch // 2 + 6)):
+    print("chunk", k, np.round(pc[k], 1))
+for n in list(range(0, 6)) + list(range(N // 2, N // 2 + 6)):
+    print("px", n, np.round(cp[n], 1))
+print("raw consumer rows", raw12[N // 2].astype(np.int64), raw12[N // 2 + 1].astype(np.int64))
+nz = np.nonzero(raw12[:, 0])[0]
+print("nonzero consumer rows:", len(nz), nz[:5], nz[-5:] if len(nz) else None)
