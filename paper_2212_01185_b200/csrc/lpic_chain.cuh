@@ -1,0 +1,336 @@
+// lpic_chain.cuh -- the decoder's on-chain table builder + symbol search.
+//
+// One quantised CDF table (kernels._quantized_cdf, kernels.py:250-293, fed
+// by the g/b branch of kernels._channel_mixture, kernels.py:212-247) and the
+// range-decoder symbol lookup (coder.py:98-106) per call, built by the 4
+// chain warps of the consumer CTA (128 threads).  This is the critical path
+// of the whole decoder (two calls per pixel, SURVEY §7 hard part 3); it is
+// laid out for latency and instruction count, with three barriers:
+//
+//   P  thread t: CDF at the upper edges of bins 2t, 2t+1 for every component
+//      (2K interleaved Phi chains, phi_gauss_vec); lane 31 -> edge slot;
+//      barrier E; PMF with the reference's per-component order and d > 0
+//      rule; exact fixed-point warp partial of the total; barrier T
+//   Q  scale, floor, m = f + 1, remainder fr = v - f, 5-bit remainder digit
+//      d = floor(32 fr); per warp: exclusive prefix of m, and for every
+//      digit value b (lane b) the lanes whose bins have digit b (ten
+//      ballots, no atomics, no zeroing); barrier A
+//   S  every warp redundantly (so no further barrier), lane l owning bins
+//      8l..8l+7: deficit; the digit bucket B holding the deficit-th largest
+//      remainder (suffix sums, bit-sliced over lanes); if B is split, its
+//      ~8 members are compacted one per lane and ranked exactly (remainder
+//      desc, index asc == the reference's stable argsort of f - v,
+//      kernels.py:286-290); cdf = prefix of m + prefix of the +1s; symbol
+//      search against the target.
+//
+// The arithmetic is bin-for-bin identical to the warp builder (lpic_cdf.cuh
+// warp_table), so encoder and decoder agree (scripts/ubench_chain.cu checks
+// it on 288k random tables; tests/test_gpu_parity.py end to end).
+#pragma once
+#include "lpic_cdf.cuh"
+
+namespace lpic {
+
+constexpr int CH_THREADS = 128;
+constexpr int CH_WARPS = 4;
+
+// barrier of the 128 chain threads (named barrier 1; loader/publisher never join)
+__device__ __forceinline__ void chain_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+struct ChainSmem {
+    alignas(16) double frac[256];                 // remainders v - f (selection keys)
+    alignas(16) uint32_t mpre[256];               // in-warp exclusive prefix of m (warp = bin >> 6)
+    alignas(16) uint32_t mpk[CH_THREADS];         // m of bins 2t | 2t+1 << 16
+    alignas(16) uint8_t dig[256];                 // remainder digits floor(32 fr)
+    alignas(16) uint8_t dig2[256];                // second digits floor(1024 fr) & 31 (0xFF: not in bucket B)
+    alignas(16) uint2 bmask[CH_WARPS][32];        // [warp][digit] = lanes with that digit (bin slot 0, slot 1)
+    alignas(16) uint2 bmask2[CH_WARPS][32];       // the same for the second digit, members of B only
+    alignas(16) unsigned long long wq[CH_WARPS];  // per-warp fixed-point PMF sums
+    alignas(16) int wm[CH_WARPS];                 // per-warp sums of m
+    alignas(16) double wedge[CH_WARPS][KMAX];     // each warp's last upper-edge CDF value per component
+};
+
+// key order of the reference's deficit selection: larger remainder first,
+// ties to the lower bin index
+__device__ __forceinline__ bool beats(double fa, int ja, double fb, int jb) {
+    return fa > fb || (fa == fb && ja < jb);
+}
+
+// optional phase timestamps (microbenchmarks only): define LPIC_CHAIN_PROF to
+// a __shared__ long long accumulator array before including this header
+#ifdef LPIC_CHAIN_PROF
+#define CHP(i) do { if (threadIdx.x == 0) { long long _c = clock64(); LPIC_CHAIN_PROF[i] += _c - _chp; _chp = _c; } } while (0)
+#define CHP0 long long _chp = clock64()
+#else
+#define CHP(i) do {} while (0)
+#define CHP0 do {} while (0)
+#endif
+
+// sum over the lanes selected by `mask` of a small per-lane count, via
+// bit-sliced ballots (BITS bits of the count)
+template <int BITS>
+__device__ __forceinline__ int lanes_sum_masked(int c, uint32_t mask) {
+    int s = 0;
+#pragma unroll
+    for (int j = 0; j < BITS; j++) s += __popc(__ballot_sync(0xffffffffu, (c >> j) & 1) & mask) << j;
+    return s;
+}
+
+// 0x00/0xFF bytes of two words -> 8 bits
+__device__ __forceinline__ uint32_t bits8(uint32_t lo, uint32_t hi) {
+    return ((lo & 0x01010101u) * 0x01020408u >> 24) | (((hi & 0x01010101u) * 0x01020408u >> 24) << 4);
+}
+
+// lanes whose 5-bit digit equals this lane's index
+__device__ __forceinline__ uint32_t digit_lanes(int d, const uint32_t (&inv)[5]) {
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < 5; j++) m &= __ballot_sync(0xffffffffu, (d >> j) & 1) ^ inv[j];
+    return m;
+}
+
+// KU > 0: compile-time component count; KU == 0: runtime K (<= KMAX)
+template <int KU, bool BLUE>
+__device__ __forceinline__ void chain_table(const double* __restrict__ pi, const double* __restrict__ inv,
+                                            const float* __restrict__ mu0, const float* __restrict__ t1,
+                                            const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
+                                            const CdfConsts* __restrict__ cc, ChainSmem* __restrict__ cs,
+                                            uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
+                                            int32_t* trace_row) {
+    constexpr int KC = KU > 0 ? KU : KMAX;
+    const int K = KU > 0 ? KU : Kr;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int k0 = 2 * t;                                   // bins k0, k0 + 1
+    CHP0;
+
+    // ---- P: CDF at the upper edges of both bins, every component
+    const double e0 = cc->edges[k0 + 1], e1 = cc->edges[k0 + 2];
+    double cur[2 * KC];
+    {
+        double z[2 * KC];
+#pragma unroll
+        for (int q = 0; q < KC; q++) {
+            if (KU == 0 && q >= K) { z[2 * q] = 0.0; z[2 * q + 1] = 0.0; continue; }
+            const float m32 = BLUE ? __fadd_rn(__fadd_rn(mu0[q], __fmul_rn(t1[q], rn)), __fmul_rn(t2[q], gn))
+                                   : __fadd_rn(mu0[q], __fmul_rn(t1[q], rn));      // kernels.py:236-240
+            const double mu = (double)m32, iv = inv[q];
+            z[2 * q] = __dmul_rn(__dsub_rn(e0, mu), iv);
+            z[2 * q + 1] = __dmul_rn(__dsub_rn(e1, mu), iv);
+        }
+        if (KU > 0 && dist == 0) {
+#ifdef ABL_NOPHI
+#pragma unroll
+            for (int i = 0; i < 2 * KC; i++) cur[i] = __dmul_rn(z[i], 0.01) + 0.5;
+#else
+            phi_gauss_vec<2 * KC>(z, cur, cc->phic);
+#endif
+        } else {
+#pragma unroll
+            for (int i = 0; i < 2 * KC; i++) {
+                if (KU == 0 && i >= 2 * K) break;
+                cur[i] = cdf_value(z[i], dist, cc->phic);
+            }
+        }
+        if (k0 + 1 == 255) {
+#pragma unroll
+            for (int q = 0; q < KC; q++) cur[2 * q + 1] = 1.0;          // kernels.py:263
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int q = 0; q < KC; q++) {
+            if (KU == 0 && q >= K) break;
+            cs->wedge[w][q] = cur[2 * q + 1];
+        }
+    }
+    CHP(0);
+    chain_sync();                                                                        // E
+    CHP(1);
+    // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
+    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < KC; q++) {
+        if (KU == 0 && q >= K) break;
+        double prev = __shfl_up_sync(0xffffffffu, cur[2 * q + 1], 1);
+        if (lane == 0) prev = (w == 0) ? 0.0 : cs->wedge[w - 1][q];
+        const double d0 = __dsub_rn(cur[2 * q], prev), d1 = __dsub_rn(cur[2 * q + 1], cur[2 * q]);
+        const double piq = pi[q];
+        const double n0 = __dadd_rn(p0, __dmul_rn(piq, d0)), n1 = __dadd_rn(p1, __dmul_rn(piq, d1));
+        p0 = d0 > 0.0 ? n0 : p0;
+        p1 = d1 > 0.0 ? n1 : p1;
+    }
+    {
+        const unsigned long long wsum = fx_warp_sum(fx_bin(p0) + fx_bin(p1));
+        if (lane == 0) cs->wq[w] = wsum;
+    }
+    CHP(2);
+    chain_sync();                                                                        // T
+    CHP(3);
+
+    // ---- Q: floors, remainders, digits (kernels.py:272-285)
+    {
+        const ulonglong2 q01 = reinterpret_cast<const ulonglong2*>(cs->wq)[0];
+        const ulonglong2 q23 = reinterpret_cast<const ulonglong2*>(cs->wq)[1];
+        const double scale = cdf_scale(fx_total((q01.x + q01.y) + (q23.x + q23.y)));
+        CHP(10);
+        const double v0 = __dmul_rn(p0, scale), v1 = __dmul_rn(p1, scale);
+        double f0 = floor(v0), f1 = floor(v1);
+        f0 = f0 > CDF_FLOOR ? CDF_FLOOR : f0;
+        f1 = f1 > CDF_FLOOR ? CDF_FLOOR : f1;
+        const int m0 = (int)f0 + 1, m1 = (int)f1 + 1;
+        const double fr0 = __dsub_rn(v0, f0), fr1 = __dsub_rn(v1, f1);     // == -(f - v) exactly
+        const int d0 = min(__double2int_rz(__dmul_rn(fr0, 32.0)), 31);
+        const int d1 = min(__double2int_rz(__dmul_rn(fr1, 32.0)), 31);
+        reinterpret_cast<double2*>(cs->frac)[t] = make_double2(fr0, fr1);
+        reinterpret_cast<uint16_t*>(cs->dig)[t] = (uint16_t)(d0 | (d1 << 8));
+        cs->mpk[t] = (uint32_t)m0 | ((uint32_t)m1 << 16);
+        const int ms = __reduce_add_sync(0xffffffffu, m0 + m1);
+        uint32_t inv[5];
+#pragma unroll
+        for (int j = 0; j < 5; j++) inv[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
+        cs->bmask[w][lane] = make_uint2(digit_lanes(d0, inv), digit_lanes(d1, inv));
+        // in-warp exclusive prefix of m in bin order (bins 2t, 2t+1)
+        const uint32_t pr = (uint32_t)(m0 + m1);
+        uint32_t incl = pr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        reinterpret_cast<uint2*>(cs->mpre)[t] = make_uint2(incl - pr, incl - pr + (uint32_t)m0);
+        if (lane == 0) cs->wm[w] = ms;
+    }
+    CHP(4);
+    chain_sync();                                                                        // A
+    CHP(5);
+
+    // ---- S: lane l owns bins 8l..8l+7 (all in warp l >> 3)
+    const int4 wm4 = *reinterpret_cast<const int4*>(cs->wm);
+    const int deficit = 65536 - ((wm4.x + wm4.y) + (wm4.z + wm4.w));
+    const int lw = lane >> 3;
+    const uint32_t mbase = lw == 0 ? 0u : (lw == 1 ? (uint32_t)wm4.x : (lw == 2 ? (uint32_t)(wm4.x + wm4.y)
+                                                                                : (uint32_t)(wm4.x + wm4.y + wm4.z)));
+    const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
+    uint32_t bm = 0;                                        // bit q: bin 8l+q gets the +1
+#ifdef ABL_NOSEL
+    if (deficit > 100000) {
+#else
+    if (deficit > 0) {
+#endif
+        // level 1 -- digit counts: lane b <-> digit b
+        int B, nB, need;
+        {
+            const uint2 k0m = cs->bmask[0][lane], k1m = cs->bmask[1][lane], k2m = cs->bmask[2][lane],
+                        k3m = cs->bmask[3][lane];
+            const int cnt = (__popc(k0m.x) + __popc(k0m.y) + __popc(k1m.x) + __popc(k1m.y)) +
+                            (__popc(k2m.x) + __popc(k2m.y) + __popc(k3m.x) + __popc(k3m.y));
+            const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);      // bins with digit >= lane
+            B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));          // deficit <= 256 = S(0)
+            nB = __shfl_sync(0xffffffffu, cnt, B);
+            need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);            // 1 <= need <= nB
+        }
+        CHP(13);
+        const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
+        bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
+        const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
+        if (need == nB) {
+            bm |= mem;
+        } else {
+            // level 2 among the members of B (uniform branch): second digit,
+            // per-warp ballots over this warp's own bins, one more barrier
+            {
+                const double2 fr2 = reinterpret_cast<const double2*>(cs->frac)[t];
+                const uint16_t dd = reinterpret_cast<const uint16_t*>(cs->dig)[t];
+                const bool in0 = (dd & 0xFF) == B, in1 = (dd >> 8) == B;
+                const int e0d = (int)(__double2ull_rz(__dmul_rn(fr2.x, 1024.0)) & 31u);
+                const int e1d = (int)(__double2ull_rz(__dmul_rn(fr2.y, 1024.0)) & 31u);
+                uint32_t inv[5];
+#pragma unroll
+                for (int j = 0; j < 5; j++) inv[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
+                cs->bmask2[w][lane] = make_uint2(digit_lanes(e0d, inv) & __ballot_sync(0xffffffffu, in0),
+                                                 digit_lanes(e1d, inv) & __ballot_sync(0xffffffffu, in1));
+                reinterpret_cast<uint16_t*>(cs->dig2)[t] = (uint16_t)((in0 ? e0d : 0xFF) | ((in1 ? e1d : 0xFF) << 8));
+            }
+            chain_sync();                                                                // A2
+            int B2, n2, need2;
+            {
+                const uint2 k0m = cs->bmask2[0][lane], k1m = cs->bmask2[1][lane], k2m = cs->bmask2[2][lane],
+                            k3m = cs->bmask2[3][lane];
+                const int cnt = (__popc(k0m.x) + __popc(k0m.y) + __popc(k1m.x) + __popc(k1m.y)) +
+                                (__popc(k2m.x) + __popc(k2m.y) + __popc(k3m.x) + __popc(k3m.y));
+                const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
+                B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
+                n2 = __shfl_sync(0xffffffffu, cnt, B2);
+                need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
+            }
+            const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
+            const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
+            // non-members carry 0xFF: mask them with mem
+            bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
+            const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
+            if (need2 == n2) {
+                bm |= mem2;
+            } else {
+                // rare: exact ranks among the members of (B, B2), frac desc / index asc
+                double fr[8];
+                const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
+#pragma unroll
+                for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
+                int rank[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) rank[q] = 0;
+                uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
+                while (lanes) {
+                    const int src = __ffs(lanes) - 1;
+                    lanes &= lanes - 1;
+                    uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
+                    while (qs) {
+                        const int q2 = __ffs(qs) - 1;
+                        qs &= qs - 1;
+                        const int j = 8 * src + q2;
+                        const double f = cs->frac[j];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
+            }
+        }
+    }
+    CHP(6);
+    // ---- cdf (kernels.py:291-293) = prefix of m + prefix of the +1s; search (coder.py:104)
+    const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
+    const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
+    const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
+    const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
+    uint32_t cdf[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
+    CHP(7);
+    const int L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));   // lane 0: cdf = 0
+    int qs = 0;
+#pragma unroll
+    for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
+    const uint4 mk = reinterpret_cast<const uint4*>(cs->mpk)[lane];
+    const uint32_t mv[4] = {mk.x, mk.y, mk.z, mk.w};
+    uint32_t st_mine = cdf[0], ms_mine = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        if (q == qs) {
+            st_mine = cdf[q];
+            ms_mine = ((mv[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) + ((bm >> q) & 1u);
+        }
+    }
+    sym = 8 * L + __shfl_sync(0xffffffffu, qs, L);
+    start = __shfl_sync(0xffffffffu, st_mine, L);
+    mass = __shfl_sync(0xffffffffu, ms_mine, L);
+    if (trace_row && w == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
+        if (lane == 31) trace_row[256] = 65536;
+    }
+    CHP(9);
+}
+
+}  // namespace lpic

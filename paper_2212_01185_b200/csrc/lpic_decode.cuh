@@ -8,11 +8,12 @@
 //     -> red CDF table (warp builder) + the g/b mixture record (softmax
 //     weights, 1/s, base means, tanh coefficients).  Records go to a
 //     per-stream ring in global memory (L2-resident) with a ready flag each.
-//   consumer (cluster rank 0, 8 chain warps + 1 loader warp): the serial
-//     chain.  The loader bulk-copies record n (cp.async.bulk + mbarrier) into
-//     a 4-slot shared-memory ring; the chain decodes r from the red table,
-//     builds the green table (block builder, 256 threads), decodes g, builds
-//     blue, decodes b, writes the pixel and publishes its progress.
+//   consumer (cluster rank 0, 4 chain warps + loader + publisher warps): the
+//     serial chain.  The loader bulk-copies record n (cp.async.bulk +
+//     mbarrier) into a 4-slot shared-memory ring; the chain decodes r from
+//     the red table, builds the green table (chain builder, lpic_chain.cuh),
+//     decodes g, builds blue, decodes b; the publisher writes the pixel and
+//     publishes the stream's progress.
 //
 // Pixel (i,j) of step t is computable once pixel (i, j-1) -- the latest of
 // its taps in coding order, in step t-1 -- is decoded (all earlier steps
@@ -21,14 +22,15 @@
 // are co-resident, so the cross-CTA spin-waits cannot deadlock.
 #pragma once
 #include "lpic_cdf.cuh"
+#include "lpic_chain.cuh"
 #include "lpic_net.cuh"
 #include "lpic_rc.cuh"
 #include "lpic_sched.cuh"
 
 namespace lpic {
 
-constexpr int DEC_CHAIN_THREADS = 256;   // == NT_THREADS: the producer runs net_tile
-constexpr int DEC_THREADS = 320;        // + loader and publisher warps (consumer) / idle in the producer
+constexpr int DEC_THREADS = 256;        // == NT_THREADS (producer net_tile); consumer: 4 chain warps +
+                                        // loader + publisher warps (two idle warps exit)
 constexpr int DEC_SLOTS = 4;
 constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publisher warp
 
@@ -238,66 +240,16 @@ struct ConsumerSmem {
     uint64_t empty[DEC_SLOTS];
     uint32_t pubq[DEC_PUBQ][2];  // (i<<16|j, r|g<<8|b<<16) for the publisher
     uint32_t chain_done, pub_done;
-    double wedge[8][4];          // per-warp last upper-edge CDF values (chain_pmf)
-    BlockCdfScratch sc;
+    ChainSmem ch;
 };
 
-// Per-bin PMF of one chain table (thread k = bin k).  The K <= 4 components
-// are evaluated branch-free in one batch so their Phi latencies overlap; the
-// lower edge of a warp's first bin is the upper edge of the previous warp's
-// last bin, passed through shared memory (one team barrier instead of a
-// divergent extra evaluation).
-constexpr int CHAIN_KU = 4;
-template <bool BLUE>
-__device__ __forceinline__ double chain_pmf(const double* pi, const double* inv, const float* mu0, const float* t1,
-                                           const float* t2, float rn, float gn, int K, int dist, const CdfConsts* cc,
-                                           double (*wedge)[CHAIN_KU]) {
-    const int k = threadIdx.x, lane = k & 31, wid = k >> 5;
-    double cur[CHAIN_KU];
-    const double e_hi = cc->edges[k + 1];
-#pragma unroll
-    for (int q = 0; q < CHAIN_KU; q++) {
-        const int qq = q < K ? q : 0;                     // padded components: evaluated, then ignored
-        const float m32 = BLUE ? mu_update2(mu0[qq], t1[qq], t2[qq], rn, gn) : mu_update1(mu0[qq], t1[qq], rn);
-        const double c = cdf_value(__dmul_rn(__dsub_rn(e_hi, (double)m32), inv[qq]), dist, cc->phic);
-        cur[q] = (k == 255) ? 1.0 : c;
-    }
-    if (lane == 31) {
-#pragma unroll
-        for (int q = 0; q < CHAIN_KU; q++) wedge[wid][q] = cur[q];
-    }
-    team_sync();
-    double pmf = 0.0;
-#pragma unroll
-    for (int q = 0; q < CHAIN_KU; q++) {
-        double prev = __shfl_up_sync(0xffffffffu, cur[q], 1);
-        if (lane == 0) prev = (wid == 0) ? 0.0 : wedge[wid - 1][q];
-        const double d = __dsub_rn(cur[q], prev);
-        const double np = __dadd_rn(pmf, __dmul_rn(pi[q < K ? q : 0], d));
-        pmf = (q < K && d > 0.0) ? np : pmf;
-    }
-    for (int q = CHAIN_KU; q < K; q++) {                  // K > 4: plain loop
-        const float m32 = BLUE ? mu_update2(mu0[q], t1[q], t2[q], rn, gn) : mu_update1(mu0[q], t1[q], rn);
-        const double mu = (double)m32, iv = inv[q];
-        const double c = (k == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(e_hi, mu), iv), dist, cc->phic);
-        double prev = __shfl_up_sync(0xffffffffu, c, 1);
-        if (lane == 0) prev = (k == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[k], mu), iv), dist, cc->phic);
-        const double d = __dsub_rn(c, prev);
-        if (d > 0.0) pmf = __dadd_rn(pmf, __dmul_rn(pi[q], d));
-    }
-    return pmf;
-}
-
-__device__ __forceinline__ void chain_symbol(BlockCdfScratch* sc, uint32_t start, uint32_t mass, uint32_t target) {
-    if (start <= target && target < start + mass) { sc->sym = threadIdx.x; sc->sstart = start; sc->smass = mass; }
-}
-
-__device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
+template <int KU>
+__device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
     ConsumerSmem* cs = reinterpret_cast<ConsumerSmem*>(smem + sizeof(CdfConsts));
     unsigned char* slots = smem + ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127);
     load_consts(cc);
-    const int tid = threadIdx.x, wid = tid >> 5;
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&cs->full[s], 1); mbar_init(&cs->empty[s], 1); }
         cs->chain_done = 0; cs->pub_done = 0;
@@ -308,8 +260,8 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
     const int64_t N = P.N;
     const uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
     const uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
-    if (wid == 8) {                                   // loader warp
-        if ((tid & 31) == 0) {
+    if (wid == CH_WARPS) {                            // loader warp
+        if (lane == 0) {
             for (int64_t n = 0; n < N; n++) {
                 const int s = (int)(n % DEC_SLOTS);
                 if (n >= DEC_SLOTS) mbar_wait(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1));
@@ -325,8 +277,8 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         return;
     }
     uint8_t* im = P.images + (int64_t)img * N * 3;
-    if (wid == 9) {                                   // publisher warp: pixels -> global, progress
-        if ((tid & 31) == 0) {
+    if (wid == CH_WARPS + 1) {                        // publisher warp: pixels -> global, progress
+        if (lane == 0) {
             volatile uint32_t* done = &cs->chain_done;
             int64_t pub = 0;
             while (pub < N) {
@@ -344,10 +296,10 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         }
         return;
     }
+    if (wid > CH_WARPS + 1) return;
     RcDecoder dec;
     dec.init(P.payload + P.offs[img], P.lens[img]);
-    BlockCdfScratch* sc = &cs->sc;
-    const double* pc = cc->phic;
+    ChainSmem* ch = &cs->ch;
     for (int64_t n = 0; n < N; n++) {
         const int s = (int)(n % DEC_SLOTS);
         unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)P.n_chunks + 12 * n : nullptr;
@@ -355,47 +307,45 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
         mbar_wait(&cs->full[s], (uint32_t)((n / DEC_SLOTS) & 1));
         if (dbg && tid == 0) { dbg[1] = gtimer(); dbg[3] = clock64(); }
         const RecView rv(slots + s * P.rec_bytes, K);
-        // ---- red: table precomputed by the producer
+        int32_t* trow = P.trace_cdf ? P.trace_cdf + ((int64_t)img * N + n) * 3 * 257 : nullptr;
+        // ---- red: table precomputed by the producer; every warp searches it
         uint64_t r;
         uint32_t target = dec.target(r);
-        const uint32_t rs = rv.red[tid];
-        const uint32_t re = tid == 255 ? 65536u : (uint32_t)rv.red[tid + 1];
-        chain_symbol(sc, rs, re - rs, target);
-        team_sync();
-        const int sr = sc->sym;
-        dec.advance(r, sc->sstart, sc->smass);
+        int sr;
+        {
+            const uint4 v = reinterpret_cast<const uint4*>(rv.red)[lane];
+            const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+            int c = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) c += ((e[q] & 0xFFFFu) <= target) + ((e[q] >> 16) <= target);
+            sr = __reduce_add_sync(0xffffffffu, c) - 1;
+            const uint32_t rs = rv.red[sr];
+            const uint32_t re = sr == 255 ? 65536u : (uint32_t)rv.red[sr + 1];
+            dec.advance(r, rs, re - rs);
+            if (trow) {
+                trow[2 * tid] = rv.red[2 * tid];
+                trow[2 * tid + 1] = rv.red[2 * tid + 1];
+                if (tid == CH_THREADS - 1) trow[256] = 65536;
+            }
+        }
         const float rn = cc->lut[sr];
         if (dbg && tid == 0) dbg[4] = clock64();
         // ---- green: mu_g += tanh(alpha)*rn (kernels.py:236-237)
-        double pmf = chain_pmf<false>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, cs->wedge);
-        if (dbg && tid == 0) dbg[5] = clock64();
-        uint32_t gs, gm;
-        block_quantize(pmf, sc, gs, gm);
-        if (dbg && tid == 0) dbg[6] = clock64();
+        int sg;
+        uint32_t st, ms;
         target = dec.target(r);
-        chain_symbol(sc, gs, gm, target);
-        team_sync();
-        const int sg = sc->sym;
-        dec.advance(r, sc->sstart, sc->smass);
+        chain_table<KU, false>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, target, sg,
+                               st, ms, trow ? trow + 257 : nullptr);
+        dec.advance(r, st, ms);
         const float gn = cc->lut[sg];
+        if (dbg && tid == 0) dbg[6] = clock64();
         // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
-        pmf = chain_pmf<true>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, cs->wedge);
-        if (dbg && tid == 0) dbg[7] = clock64();
-        uint32_t bs, bm;
-        block_quantize(pmf, sc, bs, bm);
-        if (dbg && tid == 0) dbg[8] = clock64();
+        int sb;
         target = dec.target(r);
-        chain_symbol(sc, bs, bm, target);
-        if (P.trace_cdf) {
-            int32_t* row = P.trace_cdf + ((int64_t)img * N + n) * 3 * 257;
-            row[tid] = (int32_t)rs;
-            row[257 + tid] = (int32_t)gs;
-            row[514 + tid] = (int32_t)bs;
-            if (tid == 255) { row[256] = 65536; row[257 + 256] = 65536; row[514 + 256] = 65536; }
-        }
-        team_sync();
-        const int sb = sc->sym;
-        dec.advance(r, sc->sstart, sc->smass);
+        chain_table<KU, true>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, target, sb, st,
+                              ms, trow ? trow + 514 : nullptr);
+        dec.advance(r, st, ms);
+        if (dbg && tid == 0) dbg[8] = clock64();
         if (tid == 0) {
             mbar_arrive(&cs->empty[s]);
             while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ <= n) __nanosleep(20);
@@ -403,7 +353,7 @@ __device__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
             cs->pubq[n % DEC_PUBQ][1] = (uint32_t)sr | ((uint32_t)sg << 8) | ((uint32_t)sb << 16);
             __threadfence_block();
             *(volatile uint32_t*)&cs->chain_done = (uint32_t)(n + 1);
-            if (dbg) { dbg[2] = gtimer(); dbg[9] = clock64(); }
+            if (dbg) { dbg[2] = gtimer(); dbg[5] = dbg[4]; dbg[7] = dbg[6]; dbg[9] = clock64(); }
         }
     }
     if (tid == 0 && dec.status) atomicOr(P.status + img, dec.status);
@@ -413,8 +363,13 @@ template <int CP, int HH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DEC_THREADS, 1) k_decode2(DecParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int img = blockIdx.x >> 1;
-    if (cluster_rank() == 0) dec_consumer(P, img, smem);
-    else dec_producer<CP, HH>(P, img, smem);
+    if (cluster_rank() == 0) {
+        if (P.K == 3) dec_consumer<3>(P, img, smem);
+        else if (P.K == 2) dec_consumer<2>(P, img, smem);
+        else dec_consumer<0>(P, img, smem);
+    } else {
+        dec_producer<CP, HH>(P, img, smem);
+    }
 }
 
 }  // namespace lpic

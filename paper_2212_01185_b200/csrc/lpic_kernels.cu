@@ -115,7 +115,7 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
 // encoder, stage 2: three quantised CDF tables per pixel (warp builder) and
 // the coded symbol's (start, width) in coding order (codec.py:168-182)
 // ---------------------------------------------------------------------------
-constexpr int TAB_WARPS = 8;
+constexpr int TAB_WARPS = 6;
 __global__ void __launch_bounds__(TAB_WARPS * 32)
 k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
