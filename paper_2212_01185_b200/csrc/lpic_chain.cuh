@@ -333,4 +333,252 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     CHP(9);
 }
 
+// ---------------------------------------------------------------------------
+// chain_table1: the same table with 256 chain threads, ONE bin per thread
+// (8 warps, two per SM sub-partition, so warp-level parallelism hides the
+// latency that a single warp per sub-partition exposes).  Same arithmetic
+// and selection as chain_table; post-barrier work is redundant per warp.
+// ---------------------------------------------------------------------------
+constexpr int C1_THREADS = 256;
+constexpr int C1_WARPS = 8;
+__device__ __forceinline__ void chain_sync1() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct ChainSmem1 {
+    alignas(16) double frac[256];
+    alignas(16) uint32_t mpre[256];               // in-warp exclusive prefix of m (warp = bin >> 5)
+    alignas(16) uint16_t mv[256];                 // m per bin
+    alignas(16) uint8_t dig[256];
+    alignas(16) uint8_t dig2[256];
+    alignas(16) uint32_t bmask[C1_WARPS][32];
+    alignas(16) uint32_t bmask2[C1_WARPS][32];
+    alignas(16) unsigned long long wq[C1_WARPS];
+    alignas(16) int wm[C1_WARPS];
+    alignas(16) double wedge[C1_WARPS][KMAX];
+};
+
+template <int KU, bool BLUE>
+__device__ __forceinline__ void chain_table1(const double* __restrict__ pi, const double* __restrict__ inv,
+                                             const float* __restrict__ mu0, const float* __restrict__ t1,
+                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
+                                             const CdfConsts* __restrict__ cc, ChainSmem1* __restrict__ cs,
+                                             uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
+                                             int32_t* trace_row) {
+    constexpr int KC = KU > 0 ? KU : KMAX;
+    const int K = KU > 0 ? KU : Kr;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;   // bin t
+    CHP0;
+    // ---- P
+    const double e0 = cc->edges[t + 1];
+    double cur[KC];
+    {
+        double z[KC];
+#pragma unroll
+        for (int q = 0; q < KC; q++) {
+            if (KU == 0 && q >= K) { z[q] = 0.0; continue; }
+            const float m32 = BLUE ? __fadd_rn(__fadd_rn(mu0[q], __fmul_rn(t1[q], rn)), __fmul_rn(t2[q], gn))
+                                   : __fadd_rn(mu0[q], __fmul_rn(t1[q], rn));      // kernels.py:236-240
+            z[q] = __dmul_rn(__dsub_rn(e0, (double)m32), inv[q]);
+        }
+        if (KU > 0 && dist == 0) {
+            double t_[KC];
+            const double2* row[KC];
+#pragma unroll
+            for (int i = 0; i < KC; i++) row[i] = phi_row(z[i], t_[i], cc->phic);
+#pragma unroll
+            for (int i = 0; i < KC; i++) { const double2 c = row[i][LPIC_PHI_ROW / 2 - 1]; cur[i] = __fma_rn(c.y, t_[i], c.x); }
+#pragma unroll
+            for (int j = LPIC_PHI_ROW / 2 - 2; j >= 0; j--) {
+#pragma unroll
+                for (int i = 0; i < KC; i++) { const double2 c = row[i][j]; cur[i] = __fma_rn(__fma_rn(cur[i], t_[i], c.y), t_[i], c.x); }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < KC; i++) {
+                if (KU == 0 && i >= K) break;
+                cur[i] = cdf_value(z[i], dist, cc->phic);
+            }
+        }
+        if (t == 255) {
+#pragma unroll
+            for (int q = 0; q < KC; q++) cur[q] = 1.0;                   // kernels.py:263
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int q = 0; q < KC; q++) {
+            if (KU == 0 && q >= K) break;
+            cs->wedge[w][q] = cur[q];
+        }
+    }
+    CHP(0);
+    chain_sync1();                                                                       // E
+    CHP(1);
+    double p0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < KC; q++) {
+        if (KU == 0 && q >= K) break;
+        double prev = __shfl_up_sync(0xffffffffu, cur[q], 1);
+        if (lane == 0) prev = (w == 0) ? 0.0 : cs->wedge[w - 1][q];
+        const double d0 = __dsub_rn(cur[q], prev);
+        const double n0 = __dadd_rn(p0, __dmul_rn(pi[q], d0));
+        p0 = d0 > 0.0 ? n0 : p0;
+    }
+    {
+        const unsigned long long wsum = fx_warp_sum(fx_bin(p0));
+        if (lane == 0) cs->wq[w] = wsum;
+    }
+    CHP(2);
+    chain_sync1();                                                                       // T
+    CHP(3);
+    {
+        const ulonglong2 q01 = reinterpret_cast<const ulonglong2*>(cs->wq)[0];
+        const ulonglong2 q23 = reinterpret_cast<const ulonglong2*>(cs->wq)[1];
+        const ulonglong2 q45 = reinterpret_cast<const ulonglong2*>(cs->wq)[2];
+        const ulonglong2 q67 = reinterpret_cast<const ulonglong2*>(cs->wq)[3];
+        const double scale = cdf_scale(fx_total(((q01.x + q01.y) + (q23.x + q23.y)) + ((q45.x + q45.y) + (q67.x + q67.y))));
+        CHP(10);
+        const double v0 = __dmul_rn(p0, scale);
+        double f0 = floor(v0);
+        f0 = f0 > CDF_FLOOR ? CDF_FLOOR : f0;
+        const int m0 = (int)f0 + 1;
+        const double fr0 = __dsub_rn(v0, f0);
+        const int d0 = min(__double2int_rz(__dmul_rn(fr0, 32.0)), 31);
+        cs->frac[t] = fr0;
+        cs->dig[t] = (uint8_t)d0;
+        cs->mv[t] = (uint16_t)m0;
+        const int ms = __reduce_add_sync(0xffffffffu, m0);
+        uint32_t invm[5];
+#pragma unroll
+        for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
+        cs->bmask[w][lane] = digit_lanes(d0, invm);
+        uint32_t incl = (uint32_t)m0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        cs->mpre[t] = incl - (uint32_t)m0;
+        if (lane == 0) cs->wm[w] = ms;
+    }
+    CHP(4);
+    chain_sync1();                                                                       // A
+    CHP(5);
+    // ---- S: lane l owns bins 8l..8l+7 (warp l >> 2)
+    int wmv[C1_WARPS];
+    {
+        const int4 a = reinterpret_cast<const int4*>(cs->wm)[0], b = reinterpret_cast<const int4*>(cs->wm)[1];
+        wmv[0] = a.x; wmv[1] = a.y; wmv[2] = a.z; wmv[3] = a.w; wmv[4] = b.x; wmv[5] = b.y; wmv[6] = b.z; wmv[7] = b.w;
+    }
+    const int deficit = 65536 - (((wmv[0] + wmv[1]) + (wmv[2] + wmv[3])) + ((wmv[4] + wmv[5]) + (wmv[6] + wmv[7])));
+    const int lw = lane >> 2;
+    uint32_t mbase = 0;
+#pragma unroll
+    for (int v = 0; v < C1_WARPS - 1; v++) mbase += (v < lw) ? (uint32_t)wmv[v] : 0u;
+    const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
+    uint32_t bm = 0;
+    if (deficit > 0) {
+        int B, nB, need;
+        {
+            int cnt = 0;
+#pragma unroll
+            for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask[v][lane]);
+            const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
+            B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));
+            nB = __shfl_sync(0xffffffffu, cnt, B);
+            need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);
+        }
+        CHP(13);
+        const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
+        bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
+        const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
+        if (need == nB) {
+            bm |= mem;
+        } else {
+            {
+                const bool in0 = cs->dig[t] == B;
+                const int e0d = (int)(__double2ull_rz(__dmul_rn(cs->frac[t], 1024.0)) & 31u);
+                uint32_t invm[5];
+#pragma unroll
+                for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
+                cs->bmask2[w][lane] = digit_lanes(e0d, invm) & __ballot_sync(0xffffffffu, in0);
+                cs->dig2[t] = (uint8_t)(in0 ? e0d : 0xFF);
+            }
+            chain_sync1();                                                               // A2
+            int B2, n2, need2;
+            {
+                int cnt = 0;
+#pragma unroll
+                for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask2[v][lane]);
+                const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
+                B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
+                n2 = __shfl_sync(0xffffffffu, cnt, B2);
+                need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
+            }
+            const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
+            const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
+            bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
+            const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
+            if (need2 == n2) {
+                bm |= mem2;
+            } else {
+                double fr[8];
+                const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
+#pragma unroll
+                for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
+                int rank[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) rank[q] = 0;
+                uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
+                while (lanes) {
+                    const int src = __ffs(lanes) - 1;
+                    lanes &= lanes - 1;
+                    uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
+                    while (qs) {
+                        const int q2 = __ffs(qs) - 1;
+                        qs &= qs - 1;
+                        const int j = 8 * src + q2;
+                        const double f = cs->frac[j];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
+            }
+        }
+    }
+    CHP(6);
+    const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
+    const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
+    const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
+    const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
+    uint32_t cdf[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
+    CHP(7);
+    const int L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));
+    int qs = 0;
+#pragma unroll
+    for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
+    const uint4 mk = reinterpret_cast<const uint4*>(cs->mv)[lane];
+    const uint32_t mw4[4] = {mk.x, mk.y, mk.z, mk.w};
+    uint32_t st_mine = cdf[0], ms_mine = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        if (q == qs) {
+            st_mine = cdf[q];
+            ms_mine = ((mw4[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) + ((bm >> q) & 1u);
+        }
+    }
+    sym = 8 * L + __shfl_sync(0xffffffffu, qs, L);
+    start = __shfl_sync(0xffffffffu, st_mine, L);
+    mass = __shfl_sync(0xffffffffu, ms_mine, L);
+    if (trace_row && w == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
+        if (lane == 31) trace_row[256] = 65536;
+    }
+    CHP(9);
+}
+
 }  // namespace lpic

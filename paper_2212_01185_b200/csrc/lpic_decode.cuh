@@ -31,7 +31,7 @@ namespace lpic {
 
 constexpr int DEC_THREADS = 256;        // == NT_THREADS (producer net_tile); consumer: 4 chain warps +
                                         // loader + publisher warps (two idle warps exit)
-constexpr int DEC_SLOTS = 4;
+constexpr int DEC_SLOTS = 8;
 constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publisher warp
 
 struct DecParams {
@@ -95,6 +95,17 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
     return v;
 }
 __device__ __forceinline__ uint32_t ld_volatile_smem(const volatile uint32_t* p) { return *p; }
+__device__ __forceinline__ unsigned long long ld_volatile_smem64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -117,6 +128,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
     }
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return done != 0;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -238,8 +258,9 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
 struct ConsumerSmem {
     uint64_t full[DEC_SLOTS];
     uint64_t empty[DEC_SLOTS];
-    uint32_t pubq[DEC_PUBQ][2];  // (i<<16|j, r|g<<8|b<<16) for the publisher
-    uint32_t chain_done, pub_done;
+    unsigned long long pubq[DEC_PUBQ];   // tag(8) | r g b (24) | i<<16|j (32), one store per pixel
+    uint32_t ready;                      // records [0, ready) are in their slots (loader -> chain)
+    uint32_t pub_done;
     ChainSmem ch;
 };
 
@@ -252,7 +273,8 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&cs->full[s], 1); mbar_init(&cs->empty[s], 1); }
-        cs->chain_done = 0; cs->pub_done = 0;
+        cs->ready = 0; cs->pub_done = 0;
+        for (int q = 0; q < DEC_PUBQ; q++) cs->pubq[q] = ~0ull;      // tag 0xFF never matches pixel 0
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -262,34 +284,48 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
     const uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
     if (wid == CH_WARPS) {                            // loader warp
         if (lane == 0) {
+            int64_t done = 0;                         // records published to the chain via `ready`
+            // publish the copies (issued for records < issued) that have completed
+            auto publish = [&](int64_t issued) {
+                while (done < issued && mbar_test(&cs->full[done % DEC_SLOTS], (uint32_t)((done / DEC_SLOTS) & 1))) {
+                    done++;
+                    st_release_cta_u32(&cs->ready, (uint32_t)done);
+                }
+            };
             for (int64_t n = 0; n < N; n++) {
                 const int s = (int)(n % DEC_SLOTS);
-                if (n >= DEC_SLOTS) mbar_wait(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1));
+                if (n >= DEC_SLOTS) {
+                    while (!mbar_test(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1))) { publish(n); __nanosleep(256); }
+                }
                 const uint32_t* fl = flags + (n & (P.ring_size - 1));
                 uint32_t ns = 32;
-                while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+                while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { publish(n); __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 mbar_arrive_tx(&cs->full[s], (uint32_t)P.rec_bytes);
                 bulk_g2s(slots + s * P.rec_bytes, ring + (int64_t)(n & (P.ring_size - 1)) * P.rec_bytes,
                          (uint32_t)P.rec_bytes, &cs->full[s]);
+                publish(n + 1);
             }
+            while (done < N) { publish(N); __nanosleep(256); }
         }
         return;
     }
     uint8_t* im = P.images + (int64_t)img * N * 3;
     if (wid == CH_WARPS + 1) {                        // publisher warp: pixels -> global, progress
         if (lane == 0) {
-            volatile uint32_t* done = &cs->chain_done;
-            int64_t pub = 0;
-            while (pub < N) {
-                uint32_t avail = *done;
-                if ((int64_t)avail <= pub) { __nanosleep(20); continue; }
-                for (; pub < (int64_t)avail; pub++) {
-                    const volatile uint32_t* q = cs->pubq[pub % DEC_PUBQ];
-                    const uint32_t ij = q[0], rgb = q[1];
+            for (int64_t pub = 0; pub < N;) {
+                // drain every slot whose tag says it holds pixel `pub`
+                int64_t got = pub;
+                while (got < N) {
+                    const unsigned long long v = ld_volatile_smem64(&cs->pubq[got % DEC_PUBQ]);
+                    if ((uint32_t)(v >> 56) != (uint32_t)(got & 0xFF)) break;
+                    const uint32_t ij = (uint32_t)v, rgb = (uint32_t)(v >> 32) & 0xFFFFFFu;
                     uint8_t* px = im + ((int64_t)(ij >> 16) * P.W + (ij & 0xFFFF)) * 3;
                     px[0] = (uint8_t)rgb; px[1] = (uint8_t)(rgb >> 8); px[2] = (uint8_t)(rgb >> 16);
+                    got++;
                 }
+                if (got == pub) { __nanosleep(200); continue; }
+                pub = got;
                 *(volatile uint32_t*)&cs->pub_done = (uint32_t)pub;
                 st_release_u32(P.progress + img, (uint32_t)pub);
             }
@@ -300,11 +336,20 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
     RcDecoder dec;
     dec.init(P.payload + P.offs[img], P.lens[img]);
     ChainSmem* ch = &cs->ch;
+    uint32_t avail = 0;                               // records known to be in their slots
     for (int64_t n = 0; n < N; n++) {
         const int s = (int)(n % DEC_SLOTS);
         unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)P.n_chunks + 12 * n : nullptr;
         if (dbg && tid == 0) dbg[0] = gtimer();
-        mbar_wait(&cs->full[s], (uint32_t)((n / DEC_SLOTS) & 1));
+        if ((int64_t)avail <= n) {
+            // the loader publishes completed copies lazily; if it has not yet
+            // confirmed record n, wait on the copy's own mbarrier
+            avail = ld_acquire_cta_u32(&cs->ready);
+            if ((int64_t)avail <= n) {
+                mbar_wait(&cs->full[s], (uint32_t)((n / DEC_SLOTS) & 1));
+                avail = (uint32_t)(n + 1);
+            }
+        }
         if (dbg && tid == 0) { dbg[1] = gtimer(); dbg[3] = clock64(); }
         const RecView rv(slots + s * P.rec_bytes, K);
         int32_t* trow = P.trace_cdf ? P.trace_cdf + ((int64_t)img * N + n) * 3 * 257 : nullptr;
@@ -346,13 +391,13 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
                               ms, trow ? trow + 514 : nullptr);
         dec.advance(r, st, ms);
         if (dbg && tid == 0) dbg[8] = clock64();
-        if (tid == 0) {
+        if (tid == 0) {                               // (slot s was last read before the blue table's barrier A)
             mbar_arrive(&cs->empty[s]);
             while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ <= n) __nanosleep(20);
-            cs->pubq[n % DEC_PUBQ][0] = (uint32_t)rv.ij;
-            cs->pubq[n % DEC_PUBQ][1] = (uint32_t)sr | ((uint32_t)sg << 8) | ((uint32_t)sb << 16);
-            __threadfence_block();
-            *(volatile uint32_t*)&cs->chain_done = (uint32_t)(n + 1);
+            const unsigned long long v = ((unsigned long long)(n & 0xFF) << 56) |
+                                         ((unsigned long long)((uint32_t)sr | ((uint32_t)sg << 8) | ((uint32_t)sb << 16)) << 32) |
+                                         (uint32_t)rv.ij;
+            *(volatile unsigned long long*)&cs->pubq[n % DEC_PUBQ] = v;
             if (dbg) { dbg[2] = gtimer(); dbg[5] = dbg[4]; dbg[7] = dbg[6]; dbg[9] = clock64(); }
         }
     }
@@ -360,7 +405,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
 }
 
 template <int CP, int HH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DEC_THREADS, 1) k_decode2(DecParams P) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DEC_THREADS, 1) k_decode2(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int img = blockIdx.x >> 1;
     if (cluster_rank() == 0) {

@@ -152,29 +152,51 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
 }
 
 // ---------------------------------------------------------------------------
-// range-coder lanes: one warp per stream, every lane runs the same state,
-// lane 0 writes.  sw entry = start<<16 | (width-1).
+// range-coder lanes (coder.py:30-73 + the encoder loop, codec.py:178-183):
+// one warp per stream.  The coder state is a 64-bit dependency chain, so
+// lane 0 alone runs it, in a compact (not unrolled) loop -- with only one
+// stream per SM the kernel is instruction-fetch bound if the body is large.
+// The warp stages the symbol words (start<<16 | width-1, coding order)
+// 256 at a time into shared memory with coalesced loads, the next chunk
+// held in registers while lane 0 codes the current one.
 // ---------------------------------------------------------------------------
+constexpr int RC_CHUNK = 256;
 __global__ void __launch_bounds__(32)
 k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
             int64_t fixed_cnt, uint8_t* out, int64_t cap_each, int64_t* lens, int32_t* status) {
+    __shared__ uint32_t sbuf[RC_CHUNK];
     const int s = blockIdx.x, lane = threadIdx.x;
     const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
     const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    const uint32_t* p = sw + base;
     RcEncoder e;
     e.init(out + (int64_t)s * cap_each, cap_each);
-    uint32_t nxt = (lane < n) ? __ldg(sw + base + lane) : 0u;
-    for (int64_t c = 0; c < n; c += 32) {
-        const uint32_t v = nxt;
-        nxt = (c + 32 + lane < n) ? __ldg(sw + base + c + 32 + lane) : 0u;
-        const int m = (int)((n - c) < 32 ? (n - c) : 32);
-        for (int q = 0; q < m; q++) {
-            const uint32_t x = __shfl_sync(0xffffffffu, v, q);
-            e.encode(x >> 16, (x & 0xFFFFu) + 1u, lane == 0);
+    uint32_t nxt[RC_CHUNK / 32];
+#pragma unroll
+    for (int q = 0; q < RC_CHUNK / 32; q++) nxt[q] = (32 * q + lane < n) ? __ldg(p + 32 * q + lane) : 0u;
+    for (int64_t c = 0; c < n; c += RC_CHUNK) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) {
+            const int64_t k = c + RC_CHUNK + 32 * q + lane;
+            nxt[q] = (k < n) ? __ldg(p + k) : 0u;
+        }
+        if (lane == 0) {
+            const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
+            uint32_t x = sbuf[0];
+#pragma unroll 1
+            for (int k = 0; k < m; k++) {
+                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];    // next symbol, off the coder chain
+                e.encode(x >> 16, (x & 0xFFFFu) + 1u, true);
+                x = y;
+            }
         }
     }
-    const int64_t len = e.finish(lane == 0);
     if (lane == 0) {
+        const int64_t len = e.finish(true);
         lens[s] = len;
         if (e.status) atomicOr(status + s, e.status);
     }

@@ -6,8 +6,9 @@ import paper_2212_01185_b200 as P
 from paper_2212_01185_b200 import _native, synth
 H = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 W = int(sys.argv[2]) if len(sys.argv) > 2 else H
+NI = int(sys.argv[3]) if len(sys.argv) > 3 else 1      # streams decoded concurrently (stream 0 is traced)
 w, cfg = synth.baseline_weights()
-imgs = synth.batch(1, H, W)
+imgs = synth.batch(NI, H, W)
 cs = P.encode_batch(imgs, w, cfg, "wave")
 m = P.network.gpu_model(w, cfg)
 L = _native.load()
@@ -19,7 +20,7 @@ buf = torch.zeros(4 * nch + 12 * N, dtype=torch.int64, device="cuda")
 L.lpic_decode_debug(m.handle, buf.data_ptr())
 out = P.decode_batch(cs, w, cfg)
 L.lpic_decode_debug(m.handle, None)
-assert np.array_equal(out[0], imgs[0])
+assert all(np.array_equal(o, i) for o, i in zip(out, imgs))
 b = buf.cpu().numpy().astype(np.float64)
 t0 = min(b[:4 * nch][b[:4 * nch] > 0].min(), b[4 * nch:].reshape(-1, 12)[:, 0].min())
 pc = (b[:4 * nch].reshape(nch, 4) - t0) / 1e3     # us

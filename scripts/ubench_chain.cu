@@ -15,6 +15,15 @@ __shared__ long long s_prof[16];     // shared accumulator: no global latency in
 #endif
 #include "lpic_chain.cuh"
 using namespace lpic;
+#ifdef CH1
+#define CT chain_table1
+#define CSM ChainSmem1
+#define NTH 256
+#else
+#define CT chain_table
+#define CSM ChainSmem
+#define NTH 128
+#endif
 
 struct Case { float raw[36]; float rn, gn; uint32_t target; int ch; };
 
@@ -23,9 +32,9 @@ __device__ float urand(uint32_t& s, float lo, float hi) { s = hash32(s + 0x9e377
 
 // one CTA per case: warp 0 builds the reference table with warp_table, then
 // the 4 chain warps run chain_table on the same mixture record
-__global__ void __launch_bounds__(128) k_check(int ncases, int K, int dist, float scale, int* bad, int32_t* rows) {
+__global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, float scale, int* bad, int32_t* rows) {
     __shared__ __align__(16) CdfConsts cc;
-    __shared__ __align__(16) ChainSmem cs;
+    __shared__ __align__(16) CSM cs;
     __shared__ WarpCdfScratch ws;
     __shared__ float raw[12 * KMAX];
     __shared__ double pi[KMAX], inv[KMAX];
@@ -66,14 +75,14 @@ __global__ void __launch_bounds__(128) k_check(int ncases, int K, int dist, floa
             const uint32_t target = s3 & 0xFFFFu;
             int sym; uint32_t start, mass;
             if (K == 3) {
-                if (ch == 1) chain_table<3, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else chain_table<3, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<3, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<3, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             } else if (K == 2) {
-                if (ch == 1) chain_table<2, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else chain_table<2, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<2, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<2, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             } else {
-                if (ch == 1) chain_table<0, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else chain_table<0, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<0, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<0, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             }
             __syncthreads();
             // expected symbol from the reference table
@@ -94,9 +103,9 @@ __global__ void __launch_bounds__(128) k_check(int ncases, int K, int dist, floa
     }
 }
 
-__global__ void __launch_bounds__(128) k_time(int tables, long long* out) {
+__global__ void __launch_bounds__(NTH) k_time(int tables, long long* out) {
     __shared__ __align__(16) CdfConsts cc;
-    __shared__ __align__(16) ChainSmem cs;
+    __shared__ __align__(16) CSM cs;
     __shared__ double pi[4], inv[4];
     __shared__ float mu0[4], ta[4], tb[4];
     load_consts(&cc);
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(128) k_time(int tables, long long* out) {
     for (int it = 0; it < tables; it++) {
         const float rn = -1.0f + 0.001f * (it & 1023);
         int sym; uint32_t st, ms;
-        chain_table<3, true>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
+        CT<3, true>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
         acc += st + ms;
         target = (target * 2654435761u + st) & 0xFFFFu;     // dependency on the previous result
     }
@@ -136,7 +145,7 @@ int main() {
             for (int si = 0; si < 3; si++) {
                 cudaMemset(bad, 0, 8);
                 const int n = 4000;
-                k_check<<<296, 128>>>(n, Ks[ki], dist, scales[si], bad, rows);
+                k_check<<<296, NTH>>>(n, Ks[ki], dist, scales[si], bad, rows);
                 int hb[2]; cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
                 printf("check K=%d dist=%d scale=%.0f: %d / %d mismatches\n", Ks[ki], dist, scales[si], hb[0], 3 * n);
                 total_bad += hb[0];
@@ -148,8 +157,8 @@ int main() {
                         if (h[k] != h[257 + k]) { printf("  k=%d ref %d got %d\n", k, h[k], h[257 + k]); shown++; }
                 }
             }
-    k_time<<<1, 128>>>(20, d); cudaDeviceSynchronize();
-    k_time<<<1, 128>>>(4000, d);
+    k_time<<<1, NTH>>>(20, d); cudaDeviceSynchronize();
+    k_time<<<1, NTH>>>(4000, d);
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("chain_table K=3: %lld cycles per table (%s)\n", h[0], cudaGetErrorString(cudaGetLastError()));
 #ifdef PROF
