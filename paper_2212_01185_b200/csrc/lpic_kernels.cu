@@ -152,15 +152,170 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
 }
 
 // ---------------------------------------------------------------------------
-// range-coder lanes (coder.py:30-73 + the encoder loop, codec.py:178-183):
-// one warp per stream.  The coder state is a 64-bit dependency chain, so
-// lane 0 alone runs it, in a compact (not unrolled) loop -- with only one
-// stream per SM the kernel is instruction-fetch bound if the body is large.
-// The warp stages the symbol words (start<<16 | width-1, coding order)
-// 256 at a time into shared memory with coalesced loads, the next chunk
-// held in registers while lane 0 codes the current one.
+// range coder (coder.py:30-73 + the encoder loop, codec.py:178-183), in
+// parallel and byte-identical to the sequential coder.
+//
+// The coder's output is the big integer L = sum_i r_i*start_i * 256^(S-S_i)
+// (r_i = range_i >> 16, S_i = byte shifts before symbol i, S = all shifts),
+// rounded up to a multiple of 2^24 by finish() and written big-endian; the
+// reference's carry propagation is exactly the carries of that sum.  Only
+// the range sequence is inherently serial, and it depends on the widths
+// alone:
+//   1. k_rc_plan   one lane per stream runs range_{i+1} = norm((range_i >> 16)
+//                  * w_i) -- three dependent integer ops per symbol -- and
+//                  records range and byte position at every RC_CH-symbol chunk;
+//   2. k_rc_chunks one thread per chunk codes its symbols from that range with
+//                  low = 0, writing its bytes at their final position (carries
+//                  ripple inside the chunk; a carry out of its first byte is
+//                  counted), and keeps its pending 48-bit low window;
+//   3. k_rc_merge  one lane per stream adds every chunk's window and carry-outs
+//                  (rare ripples through 0xFF runs) and applies finish().
 // ---------------------------------------------------------------------------
+constexpr int RC_CH = 1024;
 constexpr int RC_CHUNK = 256;
+static_assert(RC_CH % RC_CHUNK == 0 && (RC_CH & (RC_CH - 1)) == 0, "chunk boundaries on block starts");
+
+__device__ __forceinline__ void rc_sym_load(const uint32_t* __restrict__ p, int64_t n, int64_t c, int lane,
+                                            uint32_t (&nxt)[RC_CHUNK / 32]) {
+#pragma unroll
+    for (int q = 0; q < RC_CHUNK / 32; q++) {
+        const int64_t k = c + 32 * q + lane;
+        nxt[q] = (k < n) ? __ldg(p + k) : 0u;
+    }
+}
+
+__global__ void __launch_bounds__(32)
+k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
+          int64_t fixed_cnt, int max_chunks, unsigned long long* __restrict__ Rc, int64_t* __restrict__ posc) {
+    __shared__ uint32_t sbuf[RC_CHUNK];
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
+    const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    const uint32_t* p = sw + base;
+    unsigned long long* R_out = Rc + (int64_t)s * max_chunks;
+    int64_t* P_out = posc + (int64_t)s * (max_chunks + 1);
+    uint32_t nxt[RC_CHUNK / 32];
+    rc_sym_load(p, n, 0, lane, nxt);
+    uint64_t R = RC_TOP - 1;
+    int64_t S = 0;
+    for (int64_t c = 0; c < n; c += RC_CHUNK) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
+        __syncwarp();
+        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt);
+        if (lane == 0) {
+            if ((c & (RC_CH - 1)) == 0) { R_out[c / RC_CH] = R; P_out[c / RC_CH] = S; }   // RC_CH % RC_CHUNK == 0
+            const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
+            uint32_t r = (uint32_t)(R >> 16);
+            uint32_t x = sbuf[0];
+            uint32_t sb = 0;                                   // shifts in this block
+#pragma unroll 1
+            for (int k = 0; k < m; k++) {
+                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
+                // range' = r * width; renormalise by whole bytes (sh <= 2 as r >= 2^24)
+                const uint64_t Pq = (uint64_t)r * ((x & 0xFFFFu) + 1u);
+                const uint32_t hi = (uint32_t)(Pq >> 32);
+                const uint32_t sh = (hi < 0x100u) + (hi == 0u);
+                sb += sh;
+                r = (uint32_t)(Pq >> (16 - 8 * sh));                          // (range' << 8sh) >> 16
+                x = y;
+            }
+            S += sb;
+            R = (uint64_t)r << 16;      // only r = R >> 16 matters to the next symbol
+        }
+    }
+    if (lane == 0) P_out[(n + RC_CH - 1) / RC_CH] = S;
+}
+
+// carry of +1 into byte j, rippling back over 0xFF down to `floor`; returns 1
+// if it ran past `floor` (a carry out of the region)
+__device__ __forceinline__ int rc_carry_into(uint8_t* out, int64_t j, int64_t floor) {
+    while (j >= floor && out[j] == 0xFF) { out[j] = 0; j--; }
+    if (j < floor) return 1;
+    out[j] += 1;
+    return 0;
+}
+
+__global__ void __launch_bounds__(128)
+k_rc_chunks(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
+            int64_t fixed_cnt, int n_streams, int max_chunks, const unsigned long long* __restrict__ Rc,
+            const int64_t* __restrict__ posc, uint8_t* out, int64_t cap_each, unsigned long long* __restrict__ Wc,
+            int32_t* __restrict__ cout, int32_t* status) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = (int)(gid / max_chunks), c = (int)(gid % max_chunks);
+    if (s >= n_streams) return;
+    const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    const int64_t i0 = (int64_t)c * RC_CH;
+    if (i0 >= n) return;
+    const int64_t i1 = (i0 + RC_CH < n) ? i0 + RC_CH : n;
+    const uint32_t* p = sw + (off ? off[s] : (int64_t)s * fixed_cnt);
+    uint8_t* o = out + (int64_t)s * cap_each;
+    const int64_t* P = posc + (int64_t)s * (max_chunks + 1);
+    const int64_t first = P[c];
+    int64_t e = first;
+    uint64_t low = 0, range = Rc[(int64_t)s * max_chunks + c];
+    int carries = 0;
+    for (int64_t i = i0; i < i1; i++) {
+        const uint32_t x = __ldg(p + i);
+        const uint64_t r = range >> 16;
+        low += r * (x >> 16);
+        range = r * ((x & 0xFFFFu) + 1u);
+        if (low >= RC_TOP) { low -= RC_TOP; carries += rc_carry_into(o, e - 1, first); }
+        while (range < RC_BOTTOM) {
+            if (e < cap_each) o[e] = (uint8_t)(low >> 40);
+            e++;
+            low = (low << 8) & RC_MASK;
+            range <<= 8;
+        }
+    }
+    if (e + 6 > cap_each) atomicOr(status + s, ST_CAPACITY);
+    Wc[(int64_t)s * max_chunks + c] = low;
+    cout[(int64_t)s * max_chunks + c] = carries;
+}
+
+__global__ void __launch_bounds__(32)
+k_rc_merge(const int64_t* __restrict__ off, const int64_t* __restrict__ cnt, int64_t fixed_cnt, int n_streams,
+           int max_chunks, const int64_t* __restrict__ posc, const unsigned long long* __restrict__ Wc,
+           const int32_t* __restrict__ cout, uint8_t* out, int64_t cap_each, int64_t* lens, int32_t* status) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_streams) return;
+    const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    const int nch = (int)((n + RC_CH - 1) / RC_CH);
+    const int64_t* P = posc + (int64_t)s * (max_chunks + 1);
+    uint8_t* o = out + (int64_t)s * cap_each;
+    const int64_t S = P[nch];
+    if (S + 6 > cap_each) { atomicOr(status + s, ST_CAPACITY); lens[s] = S + 3; return; }
+    // the final window region starts zeroed
+    for (int q = 0; q < 6; q++) o[S + q] = 0;
+    for (int c = 0; c < nch; c++) {
+        const int32_t co = cout[(int64_t)s * max_chunks + c];
+        for (int q = 0; q < co; q++) rc_carry_into(o, P[c] - 1, 0);
+        // chunk c's pending window at bytes [P[c+1], P[c+1]+6), big-endian
+        const uint64_t W = Wc[(int64_t)s * max_chunks + c];
+        const int64_t at = P[c + 1];
+        int carry = 0;
+        for (int q = 5; q >= 0; q--) {
+            const int v = (int)o[at + q] + (int)((W >> (8 * (5 - q))) & 0xFFu) + carry;
+            o[at + q] = (uint8_t)v;
+            carry = v >> 8;
+        }
+        if (carry) rc_carry_into(o, at - 1, 0);
+    }
+    // finish (coder.py:59-73): round the final window up to a multiple of 2^24
+    if (o[S + 3] | o[S + 4] | o[S + 5]) {
+        int carry = 1;
+        for (int q = 2; q >= 0 && carry; q--) {
+            const int v = (int)o[S + q] + 1;
+            o[S + q] = (uint8_t)v;
+            carry = v >> 8;
+        }
+        if (carry) rc_carry_into(o, S - 1, 0);
+    }
+    lens[s] = S + 3;
+}
+
+// Legacy sequential lane (kept for the explicit-stream parity entry point)
 __global__ void __launch_bounds__(32)
 k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
             int64_t fixed_cnt, uint8_t* out, int64_t cap_each, int64_t* lens, int32_t* status) {
@@ -172,24 +327,19 @@ k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, co
     RcEncoder e;
     e.init(out + (int64_t)s * cap_each, cap_each);
     uint32_t nxt[RC_CHUNK / 32];
-#pragma unroll
-    for (int q = 0; q < RC_CHUNK / 32; q++) nxt[q] = (32 * q + lane < n) ? __ldg(p + 32 * q + lane) : 0u;
+    rc_sym_load(p, n, 0, lane, nxt);
     for (int64_t c = 0; c < n; c += RC_CHUNK) {
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
         __syncwarp();
-#pragma unroll
-        for (int q = 0; q < RC_CHUNK / 32; q++) {
-            const int64_t k = c + RC_CHUNK + 32 * q + lane;
-            nxt[q] = (k < n) ? __ldg(p + k) : 0u;
-        }
+        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt);
         if (lane == 0) {
             const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
             uint32_t x = sbuf[0];
 #pragma unroll 1
             for (int k = 0; k < m; k++) {
-                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];    // next symbol, off the coder chain
+                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
                 e.encode(x >> 16, (x & 0xFFFFu) + 1u, true);
                 x = y;
             }
@@ -301,6 +451,11 @@ struct lpic_model {
     int ord_H = -1, ord_W = -1, ord_mode = -1;
     // workspace
     uint32_t* d_sw = nullptr; size_t sw_cap = 0;
+    // parallel range-coder workspace (k_rc_plan / k_rc_chunks / k_rc_merge)
+    unsigned long long* d_rcR = nullptr; size_t rcR_cap = 0;
+    unsigned long long* d_rcW = nullptr; size_t rcW_cap = 0;
+    int64_t* d_rcP = nullptr; size_t rcP_cap = 0;
+    int32_t* d_rcC = nullptr; size_t rcC_cap = 0;
     float* d_raw = nullptr; size_t raw_cap = 0;
     uint8_t* d_img = nullptr; size_t img_cap = 0;
     uint8_t* d_pay = nullptr; size_t pay_cap = 0;
@@ -332,6 +487,29 @@ int ensure(T*& p, size_t& cap, size_t need) {
     size_t n = need < 64 ? 64 : need;
     if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return fail(LPIC_E_NOMEM, "cudaMalloc workspace failed");
     cap = n;
+    return 0;
+}
+
+struct RcWork {
+    unsigned long long *R, *W;
+    int64_t* P;
+    int32_t* C;
+};
+// the three-phase parallel range coder over n streams (fixed count or
+// per-stream off/cnt); max_count bounds every stream's symbol count
+int rc_encode_parallel(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt,
+                       int64_t fixed_cnt, int n, int64_t max_count, uint8_t* d_out, int64_t cap_each,
+                       int64_t* d_lens, int32_t* d_status, cudaStream_t st) {
+    const int max_chunks = (int)((max_count + RC_CH - 1) / RC_CH) > 0 ? (int)((max_count + RC_CH - 1) / RC_CH) : 1;
+    k_rc_plan<<<n, 32, 0, st>>>(d_sw, d_off, d_cnt, fixed_cnt, max_chunks, wk.R, wk.P);
+    CUDA_TRY(cudaGetLastError());
+    const int64_t threads = (int64_t)n * max_chunks;
+    k_rc_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(d_sw, d_off, d_cnt, fixed_cnt, n, max_chunks, wk.R,
+                                                                   wk.P, d_out, cap_each, wk.W, wk.C, d_status);
+    CUDA_TRY(cudaGetLastError());
+    k_rc_merge<<<(unsigned)((n + 31) / 32), 32, 0, st>>>(d_off, d_cnt, fixed_cnt, n, max_chunks, wk.P, wk.W, wk.C,
+                                                           d_out, cap_each, d_lens, d_status);
+    CUDA_TRY(cudaGetLastError());
     return 0;
 }
 
@@ -597,6 +775,7 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
     cudaFree(m->d_step_off); cudaFree(m->d_chunks); cudaFree(m->d_ring); cudaFree(m->d_flags);
     cudaFree(m->d_progress);
+    cudaFree(m->d_rcR); cudaFree(m->d_rcW); cudaFree(m->d_rcP); cudaFree(m->d_rcC);
     delete m;
     return 0;
 }
@@ -646,9 +825,23 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
                            uint8_t* d_out, int64_t cap_each, int64_t* d_len, int32_t* d_status, void* stream) {
     if (n_streams < 0 || !d_off || !d_cnt) return fail(LPIC_E_ARG, "bad argument");
     if (n_streams == 0) return 0;
-    k_rc_encode<<<n_streams, 32, 0, (cudaStream_t)stream>>>(d_sw, d_off, d_cnt, 0, d_out, cap_each, d_len, d_status);
-    CUDA_TRY(cudaGetLastError());
-    return 0;
+    // parity entry: size the workspace from the largest stream (one host sync)
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<int64_t> hc((size_t)n_streams);
+    CUDA_TRY(cudaMemcpyAsync(hc.data(), d_cnt, sizeof(int64_t) * n_streams, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t mx = 1;
+    for (int64_t c : hc) mx = c > mx ? c : mx;
+    const int64_t mc = (mx + RC_CH - 1) / RC_CH;
+    RcWork wk{};
+    CUDA_TRY(cudaMalloc(&wk.R, sizeof(unsigned long long) * n_streams * mc));
+    CUDA_TRY(cudaMalloc(&wk.W, sizeof(unsigned long long) * n_streams * mc));
+    CUDA_TRY(cudaMalloc(&wk.P, sizeof(int64_t) * n_streams * (mc + 1)));
+    CUDA_TRY(cudaMalloc(&wk.C, sizeof(int32_t) * n_streams * mc));
+    const int r = rc_encode_parallel(wk, d_sw, d_off, d_cnt, 0, n_streams, mx, d_out, cap_each, d_len, d_status, st);
+    cudaStreamSynchronize(st);
+    cudaFree(wk.R); cudaFree(wk.W); cudaFree(wk.P); cudaFree(wk.C);
+    return r;
 }
 
 int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_cdf, int64_t N, int32_t* d_syms,
@@ -674,9 +867,18 @@ int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, in
     if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
                                     d_trace_raw, d_trace_cdf, st))
         return r;
-    k_rc_encode<<<n, 32, 0, st>>>(m->d_sw, nullptr, nullptr, 3 * N, d_payload, cap_each, d_lens, d_status);
-    CUDA_TRY(cudaGetLastError());
-    m->launches = 3;
+    {
+        const int64_t mc = (3 * N + RC_CH - 1) / RC_CH;
+        if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)n * mc)) return r;
+        if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)n * mc)) return r;
+        if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)n * (mc + 1))) return r;
+        if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)n * mc)) return r;
+        RcWork wk{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC};
+        if (int r = rc_encode_parallel(wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
+                                       d_status, st))
+            return r;
+    }
+    m->launches = 5;
     return 0;
 }
 
@@ -727,7 +929,7 @@ int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, in
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(h_payload, m->d_pack, (size_t)total, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    m->launches = 3;
+    m->launches = 6;
     return 0;
 }
 
