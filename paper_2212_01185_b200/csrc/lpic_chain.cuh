@@ -90,13 +90,15 @@ __device__ __forceinline__ uint32_t digit_lanes(int d, const uint32_t (&inv)[5])
 }
 
 // KU > 0: compile-time component count; KU == 0: runtime K (<= KMAX)
+// want_sym < 0: decoder -- find the symbol whose interval holds `target`;
+// want_sym >= 0: encoder -- return that symbol's (start, mass).
 template <int KU, bool BLUE>
 __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const double* __restrict__ inv,
                                             const float* __restrict__ mu0, const float* __restrict__ t1,
                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
                                             const CdfConsts* __restrict__ cc, ChainSmem* __restrict__ cs,
                                             uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
-                                            int32_t* trace_row) {
+                                            int32_t* trace_row, int want_sym = -1) {
     constexpr int KC = KU > 0 ? KU : KMAX;
     const int K = KU > 0 ? KU : Kr;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -308,10 +310,15 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
 #pragma unroll
     for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
     CHP(7);
-    const int L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));   // lane 0: cdf = 0
-    int qs = 0;
+    int L, qs = 0;
+    if (want_sym >= 0) {
+        L = want_sym >> 3;
+        qs = want_sym & 7;
+    } else {
+        L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));         // lane 0: cdf = 0
 #pragma unroll
-    for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
+        for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
+    }
     const uint4 mk = reinterpret_cast<const uint4*>(cs->mpk)[lane];
     const uint32_t mv[4] = {mk.x, mk.y, mk.z, mk.w};
     uint32_t st_mine = cdf[0], ms_mine = 0;
