@@ -36,12 +36,36 @@ sys.path.insert(0, ROOT)
 FLOP_PER_SUBPX = 38912          # 58,368 MAC/px (network.py:145-156) * 2 / 3
 CONFIGS = {
     "c2": dict(n=24, H=512, W=768, desc="24 x 768x512 RGB (BASELINE configs[1])"),
-    "c1": dict(n=1, H=64, W=64, desc="1 x 64x64 RGB (BASELINE configs[0])"),
-    "c3": dict(n=256, H=1536, W=2048, desc="256 x 2048x1536 RGB (BASELINE configs[2])"),
-    "c4": dict(n=256, H=512, W=512, desc="8192^2 image as 256 x 512x512 tiles (BASELINE configs[3])"),
+    "c1": dict(n=1, H=64, W=64, kind="c1", desc="1 x 64x64 RGB, 1/f seed 0 beta=2 sigma=3 (BASELINE configs[0])"),
+    "c3": dict(n=32, H=1536, W=2048, desc="32 x 2048x1536 RGB per GPU = 256 over 8 GPUs (BASELINE configs[2])"),
+    "c4": dict(n=256, H=512, W=512, kind="tiles", scaling="strong",
+               desc="one 8192x8192 RGB image as 256 independently coded 512x512 tiles, sharded over GPUs "
+                    "(BASELINE configs[3])"),
+    "c5-1": dict(n=1, H=256, W=256, desc="1 x 256x256 RGB (BASELINE configs[4])"),
+    "c5-8": dict(n=8, H=256, W=256, desc="8 x 256x256 RGB (BASELINE configs[4])"),
     "c5-64": dict(n=64, H=256, W=256, desc="64 x 256x256 RGB (BASELINE configs[4])"),
     "c5-512": dict(n=512, H=256, W=256, desc="512 x 256x256 RGB (BASELINE configs[4])"),
+    "c5-4096": dict(n=4096, H=256, W=256, desc="4096 x 256x256 RGB (BASELINE configs[4])"),
 }
+
+
+def make_images(cfgd, rank: int, world: int, gray: bool):
+    """(images (n,H,W,3) u8, description) for this rank.  Weak scaling: every
+    rank codes its own images (seeds rank*n ...).  c4 (strong): one 8192^2
+    image, this rank's contiguous share of its 256 tiles."""
+    from paper_2212_01185_b200 import shard, synth, tiles
+    n, H, W = cfgd["n"], cfgd["H"], cfgd["W"]
+    kind = cfgd.get("kind", "images")
+    if kind == "c1":
+        return np.stack([synth.c1_image()])
+    if kind == "tiles":
+        big = synth.synth_1f(0, 8192, 8192)
+        grid = tiles.tile_grid(8192, 8192, H, W)
+        lo, hi = shard.shard_range(len(grid), rank, world)
+        return np.stack([big[i0:i0 + h, j0:j0 + w] for i0, j0, h, w in grid[lo:hi]])
+    if gray:
+        return np.stack([tiles.gray_to_rgb(synth.synth_1f_gray(rank * n + k, H, W)) for k in range(n)])
+    return synth.batch(n, H, W, seed0=rank * n)
 
 
 def env_int(name, default):
@@ -140,8 +164,7 @@ def run_reference(args, cfgd):
     w, cfg = synth.baseline_weights()
     n, H, W = cfgd["n"], cfgd["H"], cfgd["W"]
     threads = os.cpu_count() or 1
-    n_img = min(n, threads)
-    imgs = synth.batch(n_img, H, W)
+    imgs = make_images(cfgd, 0, 1, args.gray)[:threads]
     # payloads from the oracle encoder, sampled: encode only what we decode
     max_px = min(H * W, args.sample_px)
     payloads = oracle_payloads(w, cfg, imgs, args.mode, threads, max_px)
@@ -150,8 +173,8 @@ def run_reference(args, cfgd):
     times = [cpu_sample(w, cfg, payloads, H, W, args.mode, threads, max_px)[1] for _ in range(args.steps)]
     tot = sum(times)
     value = 3.0 * max_px * threads * args.steps / tot / 1e6
-    sample = (f"first {max_px} pixels (coding order) of {threads} concurrent 768x512 streams per step, "
-              f"one stream per host thread" if cfgd is CONFIGS["c2"] else f"first {max_px} px of {threads} streams")
+    sample = (f"first {max_px} pixels (coding order) of {threads} concurrent {W}x{H} streams per step, "
+              f"one stream per host thread (streams reused cyclically if fewer images)")
     line = {
         "metric": "decode Msubpixel/s (wavefront)", "value": value, "unit": "Msubpixel/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
@@ -181,10 +204,13 @@ def run_ours(args, cfgd):
     dev = torch.device("cuda", local)
     L = _native.require_cuda()
     w, cfg = synth.baseline_weights()
-    n, H, W = cfgd["n"], cfgd["H"], cfgd["W"]
+    H, W = cfgd["H"], cfgd["W"]
     N = H * W
     mode = P.parse_mode(args.mode)
-    imgs = synth.batch(n, H, W, seed0=rank * n)
+    imgs = make_images(cfgd, rank, world, args.gray)
+    n = imgs.shape[0]
+    strong = cfgd.get("scaling", "weak") == "strong"
+    units_per_img = N if args.gray else 3 * N          # gray: one sample per pixel (r=g=b replicated)
     m = P.network.gpu_model(w, cfg)
     stream = torch.cuda.Stream(device=dev)
     sp = int(stream.cuda_stream)
@@ -248,7 +274,10 @@ def run_ours(args, cfgd):
     if world > 1:
         dist.all_reduce(tot_dec, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot_enc, op=dist.ReduceOp.MAX)
-    subpx = 3.0 * N * n * world * args.steps
+    n_all = torch.tensor([n], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_all, op=dist.ReduceOp.SUM)
+    subpx = float(units_per_img) * int(n_all.item()) * args.steps
     dec_val = subpx / (tot_dec.item() / 1e3) / 1e6
     enc_val = subpx / (tot_enc.item() / 1e3) / 1e6
 
@@ -283,27 +312,31 @@ def run_ours(args, cfgd):
     e2e = torch.tensor([e2e_dec_s, e2e_enc_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
-    per_step_subpx = 3.0 * N * n * world
+    per_step_subpx = float(units_per_img) * int(n_all.item())
     e2e_dec = per_step_subpx / e2e[0].item() / 1e6
     e2e_enc = per_step_subpx / e2e[1].item() / 1e6
 
     peaks, peak_kind = load_peaks()
     dec_ms_step = tot_dec.item() / args.steps
-    bpsp = 8.0 * float(lens.sum()) / (3.0 * N * n)
+    bpsp = 8.0 * float(lens.sum()) / (float(units_per_img) * n)
     line = None
     if rank == 0:
-        achieved_tf = dec_val * 1e6 / world * FLOP_PER_SUBPX / 1e12
+        flop_unit = FLOP_PER_SUBPX * (3 if args.gray else 1)      # a gray pixel runs the net once for 3 sub-pixels
+        achieved_tf = dec_val * 1e6 / world * flop_unit / 1e12
+        metric = "decode Mpixel/s (grayscale, r=g=b)" if args.gray else "decode Msubpixel/s (wavefront)"
+        unit = "Mpixel/s" if args.gray else "Msubpixel/s"
         line = {
-            "metric": "decode Msubpixel/s (wavefront)", "value": dec_val, "unit": "Msubpixel/s", "n_gpus": world,
+            "metric": metric, "value": dec_val, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dec_ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": {"workload": cfgd["desc"], "images_per_gpu": n, "mode": args.mode,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": cfgd["desc"] + (" -- grayscale variant" if args.gray else ""),
+                       "images_per_gpu": n, "mode": args.mode,
                        "weights": "kaiming seed 0 (K=3,C=128,L=5,h=2)", "precision": "compat (bit-exact fp32 net)",
                        "l2": "256 MiB flush between timed steps"},
-            "encode": {"value": enc_val, "unit": "Msubpixel/s", "ms_per_step": tot_enc.item() / args.steps,
+            "encode": {"value": enc_val, "unit": unit, "ms_per_step": tot_enc.item() / args.steps,
                        "e2e": e2e_enc},
-            "bpsp": bpsp,
-            "e2e": {"value": e2e_dec, "unit": "Msubpixel/s", "h2d_bytes_per_step": int(lens.sum()) + 16 * n,
+            ("bits_per_gray_pixel" if args.gray else "bpsp"): bpsp,
+            "e2e": {"value": e2e_dec, "unit": unit, "h2d_bytes_per_step": int(lens.sum()) + 16 * n,
                     "d2h_bytes_per_step": int(3 * N * n) + 4 * n},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_tflops"],
                          "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"], "traffic": None,
@@ -335,11 +368,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
     ap.add_argument("--mode", default="wave", choices=["seq", "wave", "diag"])
     ap.add_argument("--sample-px", type=int, default=12288)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gray", action="store_true", help="grayscale variant (r=g=b replication, BASELINE configs[4])")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfgd = CONFIGS[args.config]

@@ -15,6 +15,8 @@ from .network import (Distribution, ModelConfig, Weights, causal_taps, count_par
                       forward_fc, forward_full, forward_patch, forward_taps_batch, glorot_weights,
                       kaiming_weights, leaky_relu, load_weights, normalize, normalize_value, save_weights,
                       weight_fingerprint, zero_weights)
+from .tiles import (TiledContainer, bits_per_gray_pixel, decode_gray, decode_tiled, encode_gray, encode_gray_batch,
+                    encode_tiled, gray_to_rgb, tile_grid)
 from .schedules import (Schedule, ScheduleMode, build_schedule, diagonal, parse_mode, sequential, validate,
                         wavefront)
 

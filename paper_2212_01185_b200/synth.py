@@ -51,3 +51,24 @@ def baseline_weights(cfg: ModelConfig | None = None):
     """'Kaiming seed 0' weights of the reference config."""
     cfg = cfg or ModelConfig()
     return kaiming_weights(cfg, np.random.default_rng(0)), cfg
+
+
+def synth_1f_gray(seed: int, H: int, W: int, beta=None, sigma=None, contrast: float = 40.0) -> np.ndarray:
+    """Single-channel variant (BASELINE configs[4] grayscale): one 1/f field
+    plus noise, same draw conventions as synth_1f."""
+    rng = np.random.default_rng(seed)
+    if beta is None:
+        beta = rng.uniform(1.6, 2.4)
+    if sigma is None:
+        sigma = rng.uniform(2.0, 6.0)
+    fy = np.fft.fftfreq(H)[:, None]
+    fx = np.fft.rfftfreq(W)[None, :]
+    f = np.sqrt(fx ** 2 + fy ** 2)
+    f[0, 0] = 1.0
+    amp = f ** (-beta / 2.0)
+    amp[0, 0] = 0.0
+    z = rng.standard_normal((H, W))
+    x = np.fft.irfft2(np.fft.rfft2(z) * amp, s=(H, W))
+    x = (x - x.mean()) / (x.std() + 1e-12)
+    img = x * contrast + 128.0 + rng.standard_normal((H, W)) * sigma
+    return np.clip(np.rint(img), 0, 255).astype(np.uint8)

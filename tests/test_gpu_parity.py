@@ -261,3 +261,28 @@ def test_gpu_seq_wave_same_length(P):
     for _ in range(3):
         img = rng.integers(0, 256, (*rng.integers(2, 24, 2), 3), dtype=np.uint8)
         assert len(P.encode(img, w, cfg, "seq").payload) == len(P.encode(img, w, cfg, "wave").payload)
+
+
+@pytest.mark.gpu
+def test_gpu_tiled_roundtrip_matches_oracle(P, oracle_mod):
+    """C4-style tiling: every tile is an independent reference-format stream."""
+    from paper_2212_01185_b200 import synth, tiles
+    w, cfg = make_weights("small", "glorot", 7)
+    img = synth.synth_1f(11, 40, 52)
+    tc = tiles.encode_tiled(img, w, cfg, "wave", tile=16)
+    assert len(tc.tiles) == 12
+    back = tiles.TiledContainer.from_bytes(tc.to_bytes())
+    assert np.array_equal(tiles.decode_tiled(back, w, cfg), img)
+    ow = oracle_weights(oracle_mod, w, cfg)
+    for (i0, j0, h, ww), c in zip(tiles.tile_grid(40, 52, 16, 16), tc.tiles):
+        assert c.payload == oracle_mod.encode(ow, np.ascontiguousarray(img[i0:i0 + h, j0:j0 + ww]), "wave")
+
+
+@pytest.mark.gpu
+def test_gpu_gray_roundtrip(P):
+    from paper_2212_01185_b200 import synth
+    w, cfg = make_weights("small", "glorot", 7)
+    g = synth.synth_1f_gray(5, 24, 30)
+    c = P.encode_gray(g, w, cfg, "wave")
+    assert np.array_equal(P.decode_gray(c, w, cfg), g)
+    assert 0.0 < P.bits_per_gray_pixel(c) < 3 * 8.5

@@ -191,3 +191,29 @@ def test_synthetic_generators(golden_meta):
     assert b.shape == (3, 32, 48, 3)
     corr = np.corrcoef(b[0, ..., 0].ravel().astype(float), b[0, ..., 1].ravel().astype(float))[0, 1]
     assert corr > 0.5
+
+
+def test_tile_grid_and_container_roundtrip():
+    from paper_2212_01185_b200 import tiles
+    g = tiles.tile_grid(1100, 700, 512, 512)
+    assert len(g) == 6 and g[-1] == (1024, 512, 76, 188)
+    assert sum(h * w for _, _, h, w in g) == 1100 * 700
+    conts = [P.Container(P.ScheduleMode.WAVEFRONT, 3, 0, w, h, 0x1234, bytes([k]) * (k + 3))
+             for k, (_, _, h, w) in enumerate(g)]
+    tc = tiles.TiledContainer(1100, 700, 512, 512, conts)
+    back = tiles.TiledContainer.from_bytes(tc.to_bytes())
+    assert (back.height, back.width, back.tile_h, back.tile_w) == (1100, 700, 512, 512)
+    assert [c.to_bytes() for c in back.tiles] == [c.to_bytes() for c in conts]
+    with pytest.raises(P.LpicError):
+        tiles.TiledContainer.from_bytes(tc.to_bytes()[:-1])
+    with pytest.raises(P.LpicError):
+        tiles.TiledContainer.from_bytes(b"XXXX" + tc.to_bytes()[4:])
+
+
+def test_gray_helpers():
+    g = synth.synth_1f_gray(3, 16, 20)
+    assert g.shape == (16, 20) and g.dtype == np.uint8
+    rgb = P.gray_to_rgb(g)
+    assert rgb.shape == (16, 20, 3) and np.array_equal(rgb[:, :, 1], g)
+    with pytest.raises(ValueError):
+        P.gray_to_rgb(rgb)
