@@ -88,6 +88,12 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
 int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_cdf, int64_t N,
                           int32_t* d_syms, int32_t* d_status, void* stream);
 
+/* kernels.true_symbol_probs (kernels.py:316-346): unquantised probability
+ * of each coded symbol.  d_raw (N,M) f32, d_syms (N,3) int64, d_rn/d_gn (N)
+ * f32 -> d_out (N,3) f64 */
+int lpic_true_symbol_probs(const float* d_raw, int64_t N, int M, int K, int dist, const int64_t* d_syms,
+                           const float* d_rn, const float* d_gn, double* d_out, void* stream);
+
 /* ---- codec (batch) -------------------------------------------------------
  * codec.encode (codec.py:156-190) over n same-size images.
  * d_images (n,H,W,3) u8; payload of image b -> d_payload + b*cap_each,
@@ -111,6 +117,11 @@ int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, in
 int lpic_decode_batch(lpic_model_t* m, const uint8_t* h_payload, const int64_t* h_offs,
                       const int64_t* h_lens, int n, int H, int W, int mode, uint8_t* h_images,
                       int32_t* h_status, void* stream);
+/* codec.theoretical_bpsp (codec.py:255-274): -log2 of the unquantised
+ * probability of every sub-pixel, in coding order: d_bits (n, H*W, 3) f64
+ * (theoretical_bpsp = sum / (3HW)). */
+int lpic_theoretical_bits(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, double* d_bits,
+                          void* stream);
 /* number of kernel launches issued by the last codec call (for bench accounting) */
 int lpic_last_launch_count(const lpic_model_t* m);
 

@@ -258,5 +258,42 @@ def bpsp(container: Container) -> float:
 
 
 def theoretical_bpsp(image: np.ndarray, w: Weights, cfg: ModelConfig, mode=ScheduleMode.SEQUENTIAL) -> float:
-    """Mean ideal code length (codec.py:255-274).  Not yet on the GPU path."""
-    raise NotImplementedError("theoretical_bpsp is not yet implemented on the GPU path (SURVEY 8(f) rank 2)")
+    """Mean ideal code length, -log2 P(r,g,b | context) per sub-pixel, with
+    the unquantised mixture probabilities the encoder sees (codec.py:255-274
+    of the reference; kernels.true_symbol_probs, kernels.py:316-346).  The
+    per-sub-pixel terms are computed on the GPU and summed here in coding
+    order like the reference's numpy sum."""
+    import torch
+    _check_image(image)
+    network.check_weights(w, cfg)
+    mode = parse_mode(mode)
+    _check_mode(mode, cfg)
+    H, W, _ = image.shape
+    m = network.gpu_model(w, cfg)
+    L = _native.load()
+    d_img = torch.from_numpy(np.ascontiguousarray(image)[None]).cuda()
+    d_bits = torch.empty((H * W, 3), dtype=torch.float64, device="cuda")
+    with m.lock:
+        _native.check(L.lpic_theoretical_bits(m.handle, d_img.data_ptr(), 1, H, W, int(mode), d_bits.data_ptr(),
+                                              _native.stream_ptr()), "lpic_theoretical_bits")
+    bits = d_bits.cpu().numpy()
+    return float(bits.sum() / (3.0 * H * W))
+
+
+def true_symbol_probs(raw: np.ndarray, syms: np.ndarray, rn: np.ndarray, gn: np.ndarray, K: int, dist: int) -> np.ndarray:
+    """kernels.true_symbol_probs on the GPU: raw (N, 12K) f32, syms (N, 3)
+    int, rn/gn (N) f32 -> (N, 3) float64."""
+    import torch
+    _native.require_cuda()
+    L = _native.load()
+    raw = np.ascontiguousarray(raw, np.float32)
+    N, M = raw.shape
+    d_raw = torch.from_numpy(raw).cuda()
+    d_s = torch.from_numpy(np.ascontiguousarray(syms, np.int64)).cuda()
+    d_rn = torch.from_numpy(np.ascontiguousarray(rn, np.float32)).cuda()
+    d_gn = torch.from_numpy(np.ascontiguousarray(gn, np.float32)).cuda()
+    d_out = torch.empty((N, 3), dtype=torch.float64, device="cuda")
+    _native.check(L.lpic_true_symbol_probs(d_raw.data_ptr(), N, M, K, int(dist), d_s.data_ptr(), d_rn.data_ptr(),
+                                           d_gn.data_ptr(), d_out.data_ptr(), _native.stream_ptr()),
+                  "lpic_true_symbol_probs")
+    return d_out.cpu().numpy()

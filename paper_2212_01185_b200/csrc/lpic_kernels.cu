@@ -447,6 +447,63 @@ k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, co
 }
 
 // ---------------------------------------------------------------------------
+// unquantised probability of the realised bin (kernels.true_symbol_probs,
+// kernels.py:316-346) -> theoretical_bpsp (codec.py:255-274).  Same mixture
+// and CDF arithmetic as the tables, evaluated only at the coded bin's edges.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double true_prob(const float* raw, int K, int dist, int ch, float rn, float gn, int x,
+                                            const CdfConsts* cc) {
+    double p = 0.0;
+    for (int i = 0; i < K; i++) {
+        const double pi = mix_pi(raw, K, ch, i);
+        const double inv = mix_inv(raw, K, ch, i);
+        const double mu = (double)mix_mu(raw, K, ch, i, rn, gn);
+        const double lo = (x == 0) ? 0.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[x], mu), inv), dist, cc->phic);
+        const double hi = (x == 255) ? 1.0 : cdf_value(__dmul_rn(__dsub_rn(cc->edges[x + 1], mu), inv), dist, cc->phic);
+        const double d = __dsub_rn(hi, lo);
+        if (d > 0.0) p = __dadd_rn(p, __dmul_rn(pi, d));
+    }
+    return p;
+}
+
+// explicit seam: raw (N,M), syms (N,3) int64, rn/gn (N) -> out (N,3) f64
+__global__ void __launch_bounds__(128)
+k_true_probs(const float* __restrict__ raw, int64_t N, int M, int K, int dist, const int64_t* __restrict__ syms,
+             const float* __restrict__ rn, const float* __restrict__ gn, double* __restrict__ out) {
+    __shared__ __align__(16) CdfConsts cc;
+    load_consts(&cc);
+    __syncthreads();
+    for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+        float r[12 * KMAX];
+        for (int m = 0; m < M; m++) r[m] = raw[n * M + m];
+        for (int ch = 0; ch < 3; ch++)
+            out[n * 3 + ch] = true_prob(r, K, dist, ch, ch >= 1 ? rn[n] : 0.0f, ch == 2 ? gn[n] : 0.0f,
+                                        (int)syms[n * 3 + ch], &cc);
+    }
+}
+
+// codec path: raw plane in coding order (k_enc_net) + images -> -log2 p per sub-pixel
+__global__ void __launch_bounds__(128)
+k_true_bits(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
+            const int32_t* __restrict__ order, int64_t N, int64_t total, double* __restrict__ bits) {
+    __shared__ __align__(16) CdfConsts cc;
+    load_consts(&cc);
+    __syncthreads();
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t img = g / N, nn = g - img * N;
+        float r[12 * KMAX];
+        for (int m = 0; m < M; m++) r[m] = raw[g * M + m];
+        const int32_t ij = __ldg(order + nn);
+        const uint8_t* px = images + ((int64_t)img * N + (int64_t)(ij >> 16) * W + (ij & 0xFFFF)) * 3;
+        const int s0 = px[0], s1 = px[1], s2 = px[2];
+        const float rn = cc.lut[s0], gn = cc.lut[s1];
+        bits[g * 3 + 0] = -log2(true_prob(r, K, dist, 0, 0.0f, 0.0f, s0, &cc));
+        bits[g * 3 + 1] = -log2(true_prob(r, K, dist, 1, rn, 0.0f, s1, &cc));
+        bits[g * 3 + 2] = -log2(true_prob(r, K, dist, 2, rn, gn, s2, &cc));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // parity seams
 // ---------------------------------------------------------------------------
 template <int CP, int HH>
@@ -663,6 +720,21 @@ template <int CP, int HH> struct EncodeRun {
         const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
         const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
         k_enc_tables<<<g2, TAB_WARPS * 32, 0, st>>>(raw, m->M, m->K, m->dist, d_images, W, m->d_order, N, total, sw, tc);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+};
+
+template <int CP, int HH> struct NetRun {
+    static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw, int32_t* d_status,
+                   cudaStream_t st) {
+        constexpr int TC = Taps<HH>::TC;
+        const size_t smem = net_tile_floats(CP, TC, m->MT, m->MP) * 4;
+        if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
+        const int64_t N = (int64_t)H * W;
+        dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
+        k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status,
+                                                          nullptr);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -943,6 +1015,38 @@ int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_c
     if (N < 0 || len < 0) return fail(LPIC_E_ARG, "bad argument");
     k_rc_decode_tables<<<1, 1, 0, (cudaStream_t)stream>>>(d_data, len, d_cdf, N, d_syms, d_status);
     CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int lpic_true_symbol_probs(const float* d_raw, int64_t N, int M, int K, int dist, const int64_t* d_syms,
+                           const float* d_rn, const float* d_gn, double* d_out, void* stream) {
+    if (N < 0 || K < 1 || K > KMAX || M < 12 * K || M > 12 * KMAX || (dist != 0 && dist != 1))
+        return fail(LPIC_E_ARG, "bad argument");
+    if (N == 0) return 0;
+    const int64_t blocks = (N + 127) / 128;
+    k_true_probs<<<(unsigned)(blocks < 4096 ? blocks : 4096), 128, 0, (cudaStream_t)stream>>>(d_raw, N, M, K, dist,
+                                                                                            d_syms, d_rn, d_gn, d_out);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int lpic_theoretical_bits(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, double* d_bits,
+                          void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lk(m->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = (int64_t)H * W;
+    if (int r = coding_order(m, H, W, mode, st)) return r;
+    if (int r = ensure(m->d_raw, m->raw_cap, (size_t)n * N * m->M)) return r;
+    if (int r = ensure(m->d_status, m->status_cap, (size_t)n)) return r;
+    CUDA_TRY(cudaMemsetAsync(m->d_status, 0, sizeof(int32_t) * n, st));
+    if (int r = dispatch<NetRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_status, st)) return r;
+    const int64_t total = N * n, blocks = (total + 127) / 128;
+    k_true_bits<<<(unsigned)(blocks < 8192 ? blocks : 8192), 128, 0, st>>>(m->d_raw, m->M, m->K, m->dist, d_images, W,
+                                                                          m->d_order, N, total, d_bits);
+    CUDA_TRY(cudaGetLastError());
+    m->launches = 2;
     return 0;
 }
 
