@@ -34,8 +34,9 @@ namespace lpic {
 constexpr int CH_THREADS = 128;
 constexpr int CH_WARPS = 4;
 
-// barrier of the 128 chain threads (named barrier 1; loader/publisher never join)
-__device__ __forceinline__ void chain_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// barrier of the 128 threads of one chain (named barrier `id`; loader and
+// publisher warps never join; a CTA may run several chains, each on its own id)
+__device__ __forceinline__ void chain_sync(int id = 1) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 struct ChainSmem {
     alignas(16) double frac[256];                 // remainders v - f (selection keys)
@@ -98,10 +99,10 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
                                             const CdfConsts* __restrict__ cc, ChainSmem* __restrict__ cs,
                                             uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
-                                            int32_t* trace_row, int want_sym = -1) {
+                                            int32_t* trace_row, int want_sym = -1, int bar = 1) {
     constexpr int KC = KU > 0 ? KU : KMAX;
     const int K = KU > 0 ? KU : Kr;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x & (CH_THREADS - 1), lane = t & 31, w = t >> 5;   // chain-local thread
     const int k0 = 2 * t;                                   // bins k0, k0 + 1
     CHP0;
 
@@ -146,7 +147,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         }
     }
     CHP(0);
-    chain_sync();                                                                        // E
+    chain_sync(bar);                                                                        // E
     CHP(1);
     // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
     double p0 = 0.0, p1 = 0.0;
@@ -166,7 +167,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         if (lane == 0) cs->wq[w] = wsum;
     }
     CHP(2);
-    chain_sync();                                                                        // T
+    chain_sync(bar);                                                                        // T
     CHP(3);
 
     // ---- Q: floors, remainders, digits (kernels.py:272-285)
@@ -203,7 +204,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         if (lane == 0) cs->wm[w] = ms;
     }
     CHP(4);
-    chain_sync();                                                                        // A
+    chain_sync(bar);                                                                        // A
     CHP(5);
 
     // ---- S: lane l owns bins 8l..8l+7 (all in warp l >> 3)
@@ -253,7 +254,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                                                  digit_lanes(e1d, inv) & __ballot_sync(0xffffffffu, in1));
                 reinterpret_cast<uint16_t*>(cs->dig2)[t] = (uint16_t)((in0 ? e0d : 0xFF) | ((in1 ? e1d : 0xFF) << 8));
             }
-            chain_sync();                                                                // A2
+            chain_sync(bar);                                                                // A2
             int B2, n2, need2;
             {
                 const uint2 k0m = cs->bmask2[0][lane], k1m = cs->bmask2[1][lane], k2m = cs->bmask2[2][lane],
@@ -361,6 +362,7 @@ struct ChainSmem1 {
     alignas(16) unsigned long long wq[C1_WARPS];
     alignas(16) int wm[C1_WARPS];
     alignas(16) double wedge[C1_WARPS][KMAX];
+    uint32_t res[4];                              // (sym, start, mass) for warps 4-7
 };
 
 template <int KU, bool BLUE>
@@ -369,7 +371,7 @@ __device__ __forceinline__ void chain_table1(const double* __restrict__ pi, cons
                                              const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
                                              const CdfConsts* __restrict__ cc, ChainSmem1* __restrict__ cs,
                                              uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
-                                             int32_t* trace_row) {
+                                             int32_t* trace_row, int want_sym = -1) {
     constexpr int KC = KU > 0 ? KU : KMAX;
     const int K = KU > 0 ? KU : Kr;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;   // bin t
@@ -470,121 +472,133 @@ __device__ __forceinline__ void chain_table1(const double* __restrict__ pi, cons
     CHP(4);
     chain_sync1();                                                                       // A
     CHP(5);
-    // ---- S: lane l owns bins 8l..8l+7 (warp l >> 2)
+    // ---- S, part 1 (all 8 warps): deficit, the level-1 threshold digit, and
+    // -- if that bucket is split -- the level-2 digit masks of each warp's bins
     int wmv[C1_WARPS];
     {
         const int4 a = reinterpret_cast<const int4*>(cs->wm)[0], b = reinterpret_cast<const int4*>(cs->wm)[1];
         wmv[0] = a.x; wmv[1] = a.y; wmv[2] = a.z; wmv[3] = a.w; wmv[4] = b.x; wmv[5] = b.y; wmv[6] = b.z; wmv[7] = b.w;
     }
     const int deficit = 65536 - (((wmv[0] + wmv[1]) + (wmv[2] + wmv[3])) + ((wmv[4] + wmv[5]) + (wmv[6] + wmv[7])));
-    const int lw = lane >> 2;
-    uint32_t mbase = 0;
-#pragma unroll
-    for (int v = 0; v < C1_WARPS - 1; v++) mbase += (v < lw) ? (uint32_t)wmv[v] : 0u;
-    const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
-    uint32_t bm = 0;
+    int B = 0, nB = 0, need = 0;
     if (deficit > 0) {
-        int B, nB, need;
-        {
-            int cnt = 0;
+        int cnt = 0;
 #pragma unroll
-            for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask[v][lane]);
-            const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
-            B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));
-            nB = __shfl_sync(0xffffffffu, cnt, B);
-            need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);
-        }
-        CHP(13);
-        const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
-        bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
-        const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
-        if (need == nB) {
-            bm |= mem;
-        } else {
-            {
-                const bool in0 = cs->dig[t] == B;
-                const int e0d = (int)(__double2ull_rz(__dmul_rn(cs->frac[t], 1024.0)) & 31u);
-                uint32_t invm[5];
+        for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask[v][lane]);
+        const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
+        B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));
+        nB = __shfl_sync(0xffffffffu, cnt, B);
+        need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);
+        if (need < nB) {                                   // uniform across the CTA
+            const bool in0 = cs->dig[t] == B;
+            const int e0d = (int)(__double2ull_rz(__dmul_rn(cs->frac[t], 1024.0)) & 31u);
+            uint32_t invm[5];
 #pragma unroll
-                for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
-                cs->bmask2[w][lane] = digit_lanes(e0d, invm) & __ballot_sync(0xffffffffu, in0);
-                cs->dig2[t] = (uint8_t)(in0 ? e0d : 0xFF);
-            }
+            for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
+            cs->bmask2[w][lane] = digit_lanes(e0d, invm) & __ballot_sync(0xffffffffu, in0);
+            cs->dig2[t] = (uint8_t)(in0 ? e0d : 0xFF);
             chain_sync1();                                                               // A2
-            int B2, n2, need2;
-            {
-                int cnt = 0;
+        }
+    }
+    CHP(13);
+    // ---- S, part 2 (warps 0-3, redundantly): lane l owns bins 8l..8l+7 (warp l >> 2)
+    if (w < 4) {
+        const int lw = lane >> 2;
+        uint32_t mbase = 0;
 #pragma unroll
-                for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask2[v][lane]);
-                const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
-                B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
-                n2 = __shfl_sync(0xffffffffu, cnt, B2);
-                need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
-            }
-            const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
-            const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
-            bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
-            const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
-            if (need2 == n2) {
-                bm |= mem2;
+        for (int v = 0; v < C1_WARPS - 1; v++) mbase += (v < lw) ? (uint32_t)wmv[v] : 0u;
+        const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
+        uint32_t bm = 0;
+        if (deficit > 0) {
+            const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
+            bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
+            const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
+            if (need == nB) {
+                bm |= mem;
             } else {
-                double fr[8];
-                const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
+                int B2, n2, need2;
+                {
+                    int cnt = 0;
 #pragma unroll
-                for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
-                int rank[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) rank[q] = 0;
-                uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
-                while (lanes) {
-                    const int src = __ffs(lanes) - 1;
-                    lanes &= lanes - 1;
-                    uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
-                    while (qs) {
-                        const int q2 = __ffs(qs) - 1;
-                        qs &= qs - 1;
-                        const int j = 8 * src + q2;
-                        const double f = cs->frac[j];
-#pragma unroll
-                        for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
-                    }
+                    for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask2[v][lane]);
+                    const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
+                    B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
+                    n2 = __shfl_sync(0xffffffffu, cnt, B2);
+                    need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
                 }
+                const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
+                const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
+                bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
+                const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
+                if (need2 == n2) {
+                    bm |= mem2;
+                } else {
+                    double fr[8];
+                    const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
 #pragma unroll
-                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
+                    for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
+                    int rank[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) rank[q] = 0;
+                    uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
+                    while (lanes) {
+                        const int src = __ffs(lanes) - 1;
+                        lanes &= lanes - 1;
+                        uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
+                        while (qs) {
+                            const int q2 = __ffs(qs) - 1;
+                            qs &= qs - 1;
+                            const int j = 8 * src + q2;
+                            const double f = cs->frac[j];
+#pragma unroll
+                            for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
+                }
             }
         }
-    }
-    CHP(6);
-    const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
-    const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
-    const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
-    const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
-    uint32_t cdf[8];
+        CHP(6);
+        const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
+        const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
+        const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
+        const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
+        uint32_t cdf[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
-    CHP(7);
-    const int L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));
-    int qs = 0;
+        for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
+        CHP(7);
+        int L, qs = 0;
+        if (want_sym >= 0) {
+            L = want_sym >> 3;
+            qs = want_sym & 7;
+        } else {
+            L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));
 #pragma unroll
-    for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
-    const uint4 mk = reinterpret_cast<const uint4*>(cs->mv)[lane];
-    const uint32_t mw4[4] = {mk.x, mk.y, mk.z, mk.w};
-    uint32_t st_mine = cdf[0], ms_mine = 0;
+            for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
+        }
+        const uint4 mk = reinterpret_cast<const uint4*>(cs->mv)[lane];
+        const uint32_t mw4[4] = {mk.x, mk.y, mk.z, mk.w};
+        uint32_t st_mine = cdf[0], ms_mine = 0;
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-        if (q == qs) {
-            st_mine = cdf[q];
-            ms_mine = ((mw4[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) + ((bm >> q) & 1u);
+        for (int q = 0; q < 8; q++) {
+            if (q == qs) {
+                st_mine = cdf[q];
+                ms_mine = ((mw4[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) + ((bm >> q) & 1u);
+            }
+        }
+        sym = 8 * L + __shfl_sync(0xffffffffu, qs, L);
+        start = __shfl_sync(0xffffffffu, st_mine, L);
+        mass = __shfl_sync(0xffffffffu, ms_mine, L);
+        if (w == 0 && lane == 0) { cs->res[0] = (uint32_t)sym; cs->res[1] = start; cs->res[2] = mass; }
+        if (trace_row && w == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
+            if (lane == 31) trace_row[256] = 65536;
         }
     }
-    sym = 8 * L + __shfl_sync(0xffffffffu, qs, L);
-    start = __shfl_sync(0xffffffffu, st_mine, L);
-    mass = __shfl_sync(0xffffffffu, ms_mine, L);
-    if (trace_row && w == 0) {
-#pragma unroll
-        for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
-        if (lane == 31) trace_row[256] = 65536;
-    }
+    chain_sync1();                                                                       // R
+    if (w >= 4) { sym = (int)cs->res[0]; start = cs->res[1]; mass = cs->res[2]; }
     CHP(9);
 }
 

@@ -29,13 +29,16 @@
 
 namespace lpic {
 
-constexpr int DEC_THREADS = 256;        // == NT_THREADS (producer net_tile); consumer: 4 chain warps +
-                                        // loader + publisher warps (two idle warps exit)
+constexpr int DEC_MAXS = 2;             // streams per cluster (throughput mode)
+constexpr int DEC_THREADS = 384;        // (S = 2) consumer: S x (4 chain warps) + S loaders + S publishers;
+                                        // producer: net_tile on 256, the rest only join its barriers
 constexpr int DEC_SLOTS = 8;
 constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publisher warp
 
 struct DecParams {
     NetDev w;
+    int S;                       // streams per cluster (chains per consumer CTA)
+    int n;                       // streams in the launch
     int K, dist, H, W, mode, a;
     int64_t N;
     const uint8_t* payload;
@@ -169,11 +172,17 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int K = P.K;
     const int64_t N = P.N;
-    const uint8_t* im = P.images + (int64_t)img * N * 3;
-    uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
-    uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
-    const uint32_t* progress = P.progress + img;
-    for (int c = 0; c < P.n_chunks; c++) {
+    const int img0 = img;
+    // chunk-major over the cluster's S streams (same geometry, so the
+    // chains progress at similar rates and neither starves the other)
+    for (int cs_ = 0; cs_ < P.n_chunks * P.S; cs_++) {
+        const int c = cs_ / P.S;
+        img = img0 + cs_ % P.S;
+        if (img >= P.n) continue;
+        const uint8_t* im = P.images + (int64_t)img * N * 3;
+        uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
+        uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
+        const uint32_t* progress = P.progress + img;
         const int n0 = P.chunks[2 * c], npx = P.chunks[2 * c + 1];
         const int64_t n = n0 + tid;
         const bool act = tid < npx && tid < NT_TP;
@@ -236,7 +245,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
             *reinterpret_cast<int32_t*>(f + 5 * K) = (i << 16) | j;
         }
         // red tables: warp w builds the tables of pixels w, w+8, ...
-        for (int p = wid; wid < 8 && p < npx; p += 8) {
+        for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
             uint32_t start[8], mass[8];
             warp_table(nb.raw + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
@@ -264,25 +273,38 @@ struct ConsumerSmem {
     ChainSmem ch;
 };
 
-template <int KU>
-__device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned char* smem) {
+template <int KU, int NT>
+__device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
-    ConsumerSmem* cs = reinterpret_cast<ConsumerSmem*>(smem + sizeof(CdfConsts));
-    unsigned char* slots = smem + ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127);
+    const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * P.rec_bytes;
+    unsigned char* gbase = smem + ((sizeof(CdfConsts) + 127) & ~(size_t)127);
     load_consts(cc);
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&cs->full[s], 1); mbar_init(&cs->empty[s], 1); }
-        cs->ready = 0; cs->pub_done = 0;
-        for (int q = 0; q < DEC_PUBQ; q++) cs->pubq[q] = ~0ull;      // tag 0xFF never matches pixel 0
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int S = P.S;
+    if (tid < S) {
+        ConsumerSmem* c0 = reinterpret_cast<ConsumerSmem*>(gbase + tid * grp);
+        for (int s = 0; s < DEC_SLOTS; s++) { mbar_init(&c0->full[s], 1); mbar_init(&c0->empty[s], 1); }
+        c0->ready = 0; c0->pub_done = 0;
+        for (int q = 0; q < DEC_PUBQ; q++) c0->pubq[q] = ~0ull;      // tag 0xFF never matches pixel 0
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
+    // roles: warps [0, 4S) chains (group g = wid / 4), [4S, 5S) loaders, [5S, 6S) publishers
+    int g, role;
+    if (wid < 4 * S) { g = wid >> 2; role = 0; }
+    else if (wid < 5 * S) { g = wid - 4 * S; role = 1; }
+    else if (wid < 6 * S) { g = wid - 5 * S; role = 2; }
+    else return;
+    const int img = img0 + g;
+    if (img >= P.n) return;
+    ConsumerSmem* cs = reinterpret_cast<ConsumerSmem*>(gbase + g * grp);
+    unsigned char* slots = gbase + g * grp + ((sizeof(ConsumerSmem) + 127) & ~(size_t)127);
+    const int bar = 1 + g;
     const int K = P.K;
     const int64_t N = P.N;
     const uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
     const uint32_t* flags = P.flags + (int64_t)img * P.ring_size;
-    if (wid == CH_WARPS) {                            // loader warp
+    if (role == 1) {                                  // loader warp
         if (lane == 0) {
             int64_t done = 0;                         // records published to the chain via `ready`
             // publish the copies (issued for records < issued) that have completed
@@ -311,7 +333,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
         return;
     }
     uint8_t* im = P.images + (int64_t)img * N * 3;
-    if (wid == CH_WARPS + 1) {                        // publisher warp: pixels -> global, progress
+    if (role == 2) {                                  // publisher warp: pixels -> global, progress
         if (lane == 0) {
             for (int64_t pub = 0; pub < N;) {
                 // drain every slot whose tag says it holds pixel `pub`
@@ -332,7 +354,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
         }
         return;
     }
-    if (wid > CH_WARPS + 1) return;
+    const int ct = tid & (CH_THREADS - 1);            // chain-local thread
     RcDecoder dec;
     dec.init(P.payload + P.offs[img], P.lens[img]);
     ChainSmem* ch = &cs->ch;
@@ -340,7 +362,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
     for (int64_t n = 0; n < N; n++) {
         const int s = (int)(n % DEC_SLOTS);
         unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)P.n_chunks + 12 * n : nullptr;
-        if (dbg && tid == 0) dbg[0] = gtimer();
+        if (dbg && ct == 0) dbg[0] = gtimer();
         if ((int64_t)avail <= n) {
             // the loader publishes completed copies lazily; if it has not yet
             // confirmed record n, wait on the copy's own mbarrier
@@ -350,7 +372,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
                 avail = (uint32_t)(n + 1);
             }
         }
-        if (dbg && tid == 0) { dbg[1] = gtimer(); dbg[3] = clock64(); }
+        if (dbg && ct == 0) { dbg[1] = gtimer(); dbg[3] = clock64(); }
         const RecView rv(slots + s * P.rec_bytes, K);
         int32_t* trow = P.trace_cdf ? P.trace_cdf + ((int64_t)img * N + n) * 3 * 257 : nullptr;
         // ---- red: table precomputed by the producer; every warp searches it
@@ -368,30 +390,30 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
             const uint32_t re = sr == 255 ? 65536u : (uint32_t)rv.red[sr + 1];
             dec.advance(r, rs, re - rs);
             if (trow) {
-                trow[2 * tid] = rv.red[2 * tid];
-                trow[2 * tid + 1] = rv.red[2 * tid + 1];
-                if (tid == CH_THREADS - 1) trow[256] = 65536;
+                trow[2 * ct] = rv.red[2 * ct];
+                trow[2 * ct + 1] = rv.red[2 * ct + 1];
+                if (ct == CH_THREADS - 1) trow[256] = 65536;
             }
         }
         const float rn = cc->lut[sr];
-        if (dbg && tid == 0) dbg[4] = clock64();
+        if (dbg && ct == 0) dbg[4] = clock64();
         // ---- green: mu_g += tanh(alpha)*rn (kernels.py:236-237)
         int sg;
         uint32_t st, ms;
         target = dec.target(r);
         chain_table<KU, false>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, target, sg,
-                               st, ms, trow ? trow + 257 : nullptr);
+                               st, ms, trow ? trow + 257 : nullptr, -1, bar);
         dec.advance(r, st, ms);
         const float gn = cc->lut[sg];
-        if (dbg && tid == 0) dbg[6] = clock64();
+        if (dbg && ct == 0) dbg[6] = clock64();
         // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
         int sb;
         target = dec.target(r);
         chain_table<KU, true>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, target, sb, st,
-                              ms, trow ? trow + 514 : nullptr);
+                              ms, trow ? trow + 514 : nullptr, -1, bar);
         dec.advance(r, st, ms);
-        if (dbg && tid == 0) dbg[8] = clock64();
-        if (tid == 0) {                               // (slot s was last read before the blue table's barrier A)
+        if (dbg && ct == 0) dbg[8] = clock64();
+        if (ct == 0) {                                // (slot s was last read before the blue table's barrier A)
             mbar_arrive(&cs->empty[s]);
             while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ <= n) __nanosleep(20);
             const unsigned long long v = ((unsigned long long)(n & 0xFF) << 56) |
@@ -401,19 +423,21 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img, unsigned 
             if (dbg) { dbg[2] = gtimer(); dbg[5] = dbg[4]; dbg[7] = dbg[6]; dbg[9] = clock64(); }
         }
     }
-    if (tid == 0 && dec.status) atomicOr(P.status + img, dec.status);
+    if (ct == 0 && dec.status) atomicOr(P.status + img, dec.status);
 }
 
-template <int CP, int HH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DEC_THREADS, 1) k_decode2(const __grid_constant__ DecParams P) {
+// NT = 256: one stream per cluster (latency; up to 255 registers per
+// thread); NT = 384: DEC_MAXS = 2 streams per cluster (throughput)
+template <int CP, int HH, int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) k_decode2(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int img = blockIdx.x >> 1;
+    const int img0 = (blockIdx.x >> 1) * P.S;
     if (cluster_rank() == 0) {
-        if (P.K == 3) dec_consumer<3>(P, img, smem);
-        else if (P.K == 2) dec_consumer<2>(P, img, smem);
-        else dec_consumer<0>(P, img, smem);
+        if (P.K == 3) dec_consumer<3, NT>(P, img0, smem);
+        else if (P.K == 2) dec_consumer<2, NT>(P, img0, smem);
+        else dec_consumer<0, NT>(P, img0, smem);
     } else {
-        dec_producer<CP, HH>(P, img, smem);
+        dec_producer<CP, HH>(P, img0, smem);
     }
 }
 

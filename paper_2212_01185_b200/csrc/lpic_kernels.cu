@@ -777,10 +777,24 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
     return 0;
 }
 
-size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes) {
+size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S) {
     const size_t prod = sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + net_tile_floats(CP, TC, MT, MP) * 4;
-    const size_t cons = ((sizeof(CdfConsts) + sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
+    const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
+    const size_t cons = ((sizeof(CdfConsts) + 127) & ~(size_t)127) + (size_t)S * grp;
     return prod > cons ? prod : cons;
+}
+
+// streams per cluster: one (latency) until the streams outnumber the
+// co-resident clusters, then two (throughput: a stream holds a 2-SM cluster
+// at ~20-30% utilisation).  LPIC_DEC_STREAMS_PER_CLUSTER overrides.
+int dec_streams_per_cluster(int n, int device) {
+    if (const char* e = getenv("LPIC_DEC_STREAMS_PER_CLUSTER")) {
+        const int v = atoi(e);
+        if (v >= 1 && v <= DEC_MAXS) return v;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return n > sms / 2 ? 2 : 1;
 }
 
 template <int CP, int HH> struct DecodeRun {
@@ -795,8 +809,10 @@ template <int CP, int HH> struct DecodeRun {
         if (int r = ensure(m->d_progress, m->progress_cap, (size_t)n)) return r;
         CUDA_TRY(cudaMemsetAsync(m->d_flags, 0, sizeof(uint32_t) * n * m->ring_size, st));
         CUDA_TRY(cudaMemsetAsync(m->d_progress, 0, sizeof(uint32_t) * n, st));
-        const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec);
-        if (set_smem(k_decode2<CP, HH>, smem)) return LPIC_E_CUDA;
+        const int S = dec_streams_per_cluster(n, m->device);
+        const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec, S);
+        if (S == 1) { if (set_smem(k_decode2<CP, HH, 256>, smem)) return LPIC_E_CUDA; }
+        else if (set_smem(k_decode2<CP, HH, DEC_THREADS>, smem)) return LPIC_E_CUDA;
         DecParams P;
         P.w = m->net; P.K = m->K; P.dist = m->dist; P.H = H; P.W = W; P.mode = mode; P.a = sched_a(mode, W, m->h);
         P.N = (int64_t)H * W; P.payload = d_payload; P.offs = d_offs; P.lens = d_lens; P.images = d_images;
@@ -804,7 +820,9 @@ template <int CP, int HH> struct DecodeRun {
         P.n_chunks = m->n_chunks; P.ring = m->d_ring; P.flags = m->d_flags; P.progress = m->d_progress;
         P.ring_size = m->ring_size; P.rec_bytes = rec; P.trace_raw = tr; P.trace_cdf = tc;
         P.dbg = m->d_dbg;
-        k_decode2<CP, HH><<<2 * n, DEC_THREADS, smem, st>>>(P);
+        P.S = S; P.n = n;
+        if (S == 1) k_decode2<CP, HH, 256><<<2 * n, 256, smem, st>>>(P);
+        else k_decode2<CP, HH, DEC_THREADS><<<2 * ((n + S - 1) / S), DEC_THREADS, smem, st>>>(P);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
