@@ -17,14 +17,16 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblpic_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["lpic_kernels.cu"]
+SOURCES = ["lpic_kernels.cu", "lpic_decode_cp16.cu", "lpic_decode_cp32.cu", "lpic_decode_cp64.cu",
+           "lpic_decode_cp128.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
+    "-fmad=false", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-Xptxas", "-O3",
 ]
+OBJDIR = os.path.join(HERE, "build_obj")
 
 
 def _stale() -> bool:
@@ -38,13 +40,26 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit in parallel (nvcc -c), then link the
+    shared library.  Stale check covers all sources and headers."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
-    if verbose:
-        cmd[1:1] = ["-Xptxas", "-v"]
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJDIR, exist_ok=True)
+    extra = ["-Xptxas", "-v"] if verbose else []
+
+    def one(src):
+        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(one, SOURCES))
+    subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp"],
+                   check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -26,6 +26,19 @@
 #include "lpic_net.cuh"
 #include "lpic_rc.cuh"
 #include "lpic_sched.cuh"
+#include "lpic_decode_launch.h"
+
+namespace lpic {
+cudaError_t launch_decode2(int CP, int HH, int S, int n, size_t smem, cudaStream_t st, const DecParams& P) {
+    switch (CP) {
+        case 16: return launch_decode2_cp16(HH, S, n, smem, st, P);
+        case 32: return launch_decode2_cp32(HH, S, n, smem, st, P);
+        case 64: return launch_decode2_cp64(HH, S, n, smem, st, P);
+        case 128: return launch_decode2_cp128(HH, S, n, smem, st, P);
+        default: return cudaErrorInvalidValue;
+    }
+}
+}  // namespace lpic
 
 using namespace lpic;
 
@@ -811,8 +824,6 @@ template <int CP, int HH> struct DecodeRun {
         CUDA_TRY(cudaMemsetAsync(m->d_progress, 0, sizeof(uint32_t) * n, st));
         const int S = dec_streams_per_cluster(n, m->device);
         const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec, S);
-        if (S == 1) { if (set_smem(k_decode2<CP, HH, 256>, smem)) return LPIC_E_CUDA; }
-        else if (set_smem(k_decode2<CP, HH, DEC_THREADS>, smem)) return LPIC_E_CUDA;
         DecParams P;
         P.w = m->net; P.K = m->K; P.dist = m->dist; P.H = H; P.W = W; P.mode = mode; P.a = sched_a(mode, W, m->h);
         P.N = (int64_t)H * W; P.payload = d_payload; P.offs = d_offs; P.lens = d_lens; P.images = d_images;
@@ -821,9 +832,9 @@ template <int CP, int HH> struct DecodeRun {
         P.ring_size = m->ring_size; P.rec_bytes = rec; P.trace_raw = tr; P.trace_cdf = tc;
         P.dbg = m->d_dbg;
         P.S = S; P.n = n;
-        if (S == 1) k_decode2<CP, HH, 256><<<2 * n, 256, smem, st>>>(P);
-        else k_decode2<CP, HH, DEC_THREADS><<<2 * ((n + S - 1) / S), DEC_THREADS, smem, st>>>(P);
-        CUDA_TRY(cudaGetLastError());
+        // the k_decode2 instantiations live in lpic_decode_cp*.cu (compiled in parallel)
+        cudaError_t e = launch_decode2(CP, HH, S, n, smem, st, P);
+        if (e != cudaSuccess) return fail(LPIC_E_CUDA, std::string("k_decode2: ") + cudaGetErrorString(e));
         return 0;
     }
 };
