@@ -211,6 +211,7 @@ def run_ours(args, cfgd):
     n = imgs.shape[0]
     strong = cfgd.get("scaling", "weak") == "strong"
     units_per_img = N if args.gray else 3 * N          # gray: one sample per pixel (r=g=b replicated)
+    P.set_precision(args.precision)
     m = P.network.gpu_model(w, cfg)
     stream = torch.cuda.Stream(device=dev)
     sp = int(stream.cuda_stream)
@@ -331,7 +332,9 @@ def run_ours(args, cfgd):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"] + (" -- grayscale variant" if args.gray else ""),
                        "images_per_gpu": n, "mode": args.mode,
-                       "weights": "kaiming seed 0 (K=3,C=128,L=5,h=2)", "precision": "compat (bit-exact fp32 net)",
+                       "weights": "kaiming seed 0 (K=3,C=128,L=5,h=2)",
+                       "precision": ("compat (bit-exact fp32 net)" if args.precision == "compat"
+                                     else "fast (tcgen05 fp16x3 net)"),
                        "l2": "256 MiB flush between timed steps"},
             "encode": {"value": enc_val, "unit": unit, "ms_per_step": tot_enc.item() / args.steps,
                        "e2e": e2e_enc},
@@ -374,6 +377,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gray", action="store_true", help="grayscale variant (r=g=b replication, BASELINE configs[4])")
+    ap.add_argument("--precision", default="compat", choices=["compat", "fast"],
+                    help="compat: reference-exact fp32 network (default); fast: tcgen05 fp16x3 network")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfgd = CONFIGS[args.config]

@@ -13,8 +13,8 @@ from .codec import (CodecTrace, Container, bpsp, decode, decode_batch, encode, e
 from .errors import CorruptStreamError, FingerprintMismatchError, LpicError, UnsupportedImageError
 from .network import (Distribution, ModelConfig, Weights, causal_taps, count_parameters, estimate_macs,
                       forward_fc, forward_full, forward_patch, forward_taps_batch, glorot_weights,
-                      kaiming_weights, leaky_relu, load_weights, normalize, normalize_value, save_weights,
-                      weight_fingerprint, zero_weights)
+                      get_precision, kaiming_weights, leaky_relu, load_weights, normalize, normalize_value,
+                      save_weights, set_precision, weight_fingerprint, zero_weights)
 from .tiles import (TiledContainer, bits_per_gray_pixel, decode_gray, decode_tiled, encode_gray, encode_gray_batch,
                     encode_tiled, gray_to_rgb, tile_grid)
 from .schedules import (Schedule, ScheduleMode, build_schedule, diagonal, parse_mode, sequential, validate,

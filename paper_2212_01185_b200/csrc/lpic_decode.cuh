@@ -24,6 +24,7 @@
 #include "lpic_cdf.cuh"
 #include "lpic_chain.cuh"
 #include "lpic_net.cuh"
+#include "lpic_net_tc.cuh"
 #include "lpic_rc.cuh"
 #include "lpic_sched.cuh"
 
@@ -37,6 +38,8 @@ constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publish
 
 struct DecParams {
     NetDev w;
+    TcNetDev tc;                 // FAST precision network (lpic_net_tc.cuh)
+    int fast;
     int S;                       // streams per cluster (chains per consumer CTA)
     int n;                       // streams in the launch
     int K, dist, H, W, mode, a;
@@ -167,8 +170,18 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     nb.raw = nb.wbuf + ((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * P.w.MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
                                                                            : CP * P.w.MT);
     __shared__ long long s_need;
+    // FAST precision: the tensor-core tile state and a raw buffer replace the fp32 tile buffers
+    const size_t tc_off = (sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127;
+    TcSmem* tcs = reinterpret_cast<TcSmem*>(smem + tc_off);
+    float* fraw = reinterpret_cast<float*>(smem + tc_off + sizeof(TcSmem));
+    uint32_t mcnt = 0;
     load_consts(cc);
+    if (P.fast && threadIdx.x < 128) tc_init(tcs);
+    umma::fence_before();
     __syncthreads();
+    umma::fence_after();
+    if (P.fast && threadIdx.x < 128) tc_prefetch(tcs, P.tc);
+    float* rawbuf = P.fast ? fraw : nb.raw;
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int K = P.K;
     const int64_t N = P.N;
@@ -214,17 +227,33 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
             if (dbg) dbg[1] = gtimer();
         }
         __syncthreads();
-        if (act) {
-            float x[TC];
-            gather_u8<HH>(im, P.H, P.W, i, j, P.mode, cc->lut, x, LdcgU8());
+        if (P.fast) {
+            if (tid < TC_M) {                                  // warps 0-3: the tensor-core tile
+                float x[TC];
+                if (act) {
+                    gather_u8<HH>(im, P.H, P.W, i, j, P.mode, cc->lut, x, LdcgU8());
+                } else {
 #pragma unroll
-            for (int q = 0; q < TC; q++) nb.act0[q * NT_TP + tid] = x[q];
+                    for (int q = 0; q < TC; q++) x[q] = 0.0f;
+                }
+                tc_store_input<TC>(tcs, tid, x, P.tc.K[0]);
+                tc_network(tcs, P.tc, act ? fraw + tid * P.w.MP : nullptr, 1, mcnt);
+                if (cs_ + 1 < P.n_chunks * P.S) tc_prefetch(tcs, P.tc);
+            }
+            __syncthreads();
+        } else {
+            if (act) {
+                float x[TC];
+                gather_u8<HH>(im, P.H, P.W, i, j, P.mode, cc->lut, x, LdcgU8());
+#pragma unroll
+                for (int q = 0; q < TC; q++) nb.act0[q * NT_TP + tid] = x[q];
+            }
+            __syncthreads();
+            net_tile<CP, TC>(P.w, nb);
         }
-        __syncthreads();
-        net_tile<CP, TC>(P.w, nb);
         if (dbg && tid == 0) dbg[2] = gtimer();
         if (act) {
-            const float* myraw = nb.raw + tid * P.w.MP;
+            const float* myraw = rawbuf + tid * P.w.MP;
             if (P.trace_raw)
                 for (int m = 0; m < P.w.M; m++) P.trace_raw[((int64_t)img * N + n) * P.w.M + m] = myraw[m];
             // g/b mixture record (kernels.py:212-247 minus the rn/gn-dependent update)
@@ -247,7 +276,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         // red tables: warp w builds the tables of pixels w, w+8, ...
         for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
             uint32_t start[8], mass[8];
-            warp_table(nb.raw + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
+            warp_table(rawbuf + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
             uint4 v;
             v.x = (start[0] & 0xFFFFu) | (start[1] << 16); v.y = (start[2] & 0xFFFFu) | (start[3] << 16);
@@ -258,6 +287,12 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         __syncthreads();
         if (act) st_release_u32(flags + (n & (P.ring_size - 1)), (uint32_t)(n + 1));
         if (dbg && tid == 0) dbg[3] = gtimer();
+    }
+    if (P.fast) {
+        umma::fence_before();
+        __syncthreads();
+        umma::fence_after();
+        if (tid < TC_M) tc_finish(tcs);
     }
 }
 

@@ -24,6 +24,7 @@
 #include "lpic_decode.cuh"
 #include "lpic_math.cuh"
 #include "lpic_net.cuh"
+#include "lpic_net_tc.cuh"
 #include "lpic_rc.cuh"
 #include "lpic_sched.cuh"
 #include "lpic_decode_launch.h"
@@ -123,6 +124,60 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
         if (trace_raw) trace_raw[((int64_t)img * N + n0 + p) * w.M + m] = v;
     }
     if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
+// encoder, stage 1 in FAST precision: the network on the tensor cores
+// (lpic_net_tc.cuh), persistent CTAs of 128 threads over 128-pixel tiles in
+// coding order; the next tile's first two weight layers stream in while the
+// current tile's last layers run.
+// ---------------------------------------------------------------------------
+template <int HH>
+__global__ void __launch_bounds__(128, 1)
+k_enc_net_tc(const __grid_constant__ TcNetDev w, const uint8_t* __restrict__ images, int H, int W, int mode,
+             const int32_t* __restrict__ order, int64_t N, int n_img, float* __restrict__ raw_out, int32_t* status,
+             float* trace_raw) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    TcSmem* s = reinterpret_cast<TcSmem*>(smem);
+    __shared__ float lut[256];
+    constexpr int TC = Taps<HH>::TC;
+    const int tid = threadIdx.x;
+    for (int v = tid; v < 256; v += 128) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
+    tc_init(s);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const int64_t tiles_per = (N + TC_M - 1) / TC_M, total = tiles_per * n_img;
+    uint32_t mcnt = 0;
+    if ((int64_t)blockIdx.x < total) tc_prefetch(s, w);
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + tid;
+        float x[TC];
+        if (n < N) {
+            const int32_t ij = __ldg(order + n);
+            gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+        } else {
+#pragma unroll
+            for (int q = 0; q < TC; q++) x[q] = 0.0f;
+        }
+        tc_store_input<TC>(s, tid, x, w.K[0]);
+        float* row = (n < N) ? raw_out + (img * N + n) * w.M : nullptr;
+        tc_network(s, w, row, 1, mcnt);
+        if (tile + gridDim.x < total) tc_prefetch(s, w);
+        if (row) {
+            bool finite = true;
+            for (int m = 0; m < w.M; m++) {
+                const float v = row[m];
+                finite &= isfinite(v);
+                if (trace_raw) trace_raw[(img * N + n) * w.M + m] = v;
+            }
+            if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    tc_finish(s);
 }
 
 // ---------------------------------------------------------------------------
@@ -610,6 +665,10 @@ struct lpic_model {
     uint64_t fingerprint;
     float* d_w;          // one allocation for all padded tensors
     NetDev net;
+    // FAST precision: fp16 hi|lo weight blobs + padded biases (lpic_net_tc.cuh)
+    unsigned char* d_tc = nullptr;
+    TcNetDev tcnet{};
+    bool tc_ok = false;
     // cached coding order per geometry
     int32_t* d_order = nullptr;
     int ord_H = -1, ord_W = -1, ord_mode = -1;
@@ -717,16 +776,34 @@ int dispatch(int CP, int HH, A&&... args) {
     return fail(LPIC_E_UNSUPPORTED, "unsupported (C, kernel_half) instantiation");
 }
 
+template <int HH>
+int launch_enc_net_tc(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw,
+                      int32_t* d_status, float* tr, cudaStream_t st) {
+    const size_t smem = sizeof(TcSmem);
+    if (set_smem(k_enc_net_tc<HH>, smem)) return LPIC_E_CUDA;
+    const int64_t N = (int64_t)H * W, tiles = ((N + TC_M - 1) / TC_M) * n;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+    const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+    k_enc_net_tc<HH><<<grid, 128, smem, st>>>(m->tcnet, d_images, H, W, mode, m->d_order, N, n, raw, d_status, tr);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 template <int CP, int HH> struct EncodeRun {
     static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw, uint32_t* sw,
                    int32_t* d_status, float* tr, int32_t* tc, cudaStream_t st) {
         constexpr int TC = Taps<HH>::TC;
-        const size_t smem = net_tile_floats(CP, TC, m->MT, m->MP) * 4;
-        if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
         const int64_t N = (int64_t)H * W;
-        dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
-        k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status, tr);
-        CUDA_TRY(cudaGetLastError());
+        if (m->precision == LPIC_PREC_FAST) {
+            if (int r = launch_enc_net_tc<HH>(m, d_images, n, H, W, mode, raw, d_status, tr, st)) return r;
+        } else {
+            const size_t smem = net_tile_floats(CP, TC, m->MT, m->MP) * 4;
+            if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
+            dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
+            k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status, tr);
+            CUDA_TRY(cudaGetLastError());
+        }
         const int64_t total = N * n;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
@@ -790,8 +867,10 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
     return 0;
 }
 
-size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S) {
-    const size_t prod = sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + net_tile_floats(CP, TC, MT, MP) * 4;
+size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S, bool fast) {
+    const size_t prod = fast ? ((sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127) +
+                                   sizeof(TcSmem) + (size_t)NT_TP * MP * 4
+                             : sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + net_tile_floats(CP, TC, MT, MP) * 4;
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
     const size_t cons = ((sizeof(CdfConsts) + 127) & ~(size_t)127) + (size_t)S * grp;
     return prod > cons ? prod : cons;
@@ -823,7 +902,8 @@ template <int CP, int HH> struct DecodeRun {
         CUDA_TRY(cudaMemsetAsync(m->d_flags, 0, sizeof(uint32_t) * n * m->ring_size, st));
         CUDA_TRY(cudaMemsetAsync(m->d_progress, 0, sizeof(uint32_t) * n, st));
         const int S = dec_streams_per_cluster(n, m->device);
-        const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec, S);
+        const bool fast = m->precision == LPIC_PREC_FAST;
+        const size_t smem = dec_smem_bytes(CP, m->TC, m->MT, m->MP, rec, S, fast);
         DecParams P;
         P.w = m->net; P.K = m->K; P.dist = m->dist; P.H = H; P.W = W; P.mode = mode; P.a = sched_a(mode, W, m->h);
         P.N = (int64_t)H * W; P.payload = d_payload; P.offs = d_offs; P.lens = d_lens; P.images = d_images;
@@ -832,6 +912,7 @@ template <int CP, int HH> struct DecodeRun {
         P.ring_size = m->ring_size; P.rec_bytes = rec; P.trace_raw = tr; P.trace_cdf = tc;
         P.dbg = m->d_dbg;
         P.S = S; P.n = n;
+        P.fast = fast ? 1 : 0; P.tc = m->tcnet;
         // the k_decode2 instantiations live in lpic_decode_cp*.cu (compiled in parallel)
         cudaError_t e = launch_decode2(CP, HH, S, n, smem, st, P);
         if (e != cudaSuccess) return fail(LPIC_E_CUDA, std::string("k_decode2: ") + cudaGetErrorString(e));
@@ -957,6 +1038,53 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
     app(hidden_w, (size_t)NH * C * C); app(hidden_b, (size_t)NH * C);
     app(out_w, (size_t)M * C); app(out_b, M);
     m->fingerprint = lpic_fnv1a64(ser.data(), (int64_t)ser.size());
+    // FAST precision operands: per layer W_hi | W_lo (fp16, canonical K-major
+    // layout of lpic_umma.cuh) and biases padded to TC_NMAX
+    {
+        const int K0p = (TC + 15) & ~15;
+        const int nl = NH + 2;
+        if (CP <= TC_NMAX && MT <= TC_NMAX && K0p <= TC_KMAX && nl <= TC_MAXL) {
+            std::vector<int> Ns(nl), Ks(nl);
+            for (int l = 0; l < nl; l++) {
+                Ns[l] = (l == nl - 1) ? MT : CP;
+                Ks[l] = (l == 0) ? K0p : CP;
+            }
+            size_t total_b = 0;
+            std::vector<size_t> boff(nl), bias_off(nl);
+            for (int l = 0; l < nl; l++) { boff[l] = total_b; total_b += (size_t)2 * Ns[l] * Ks[l] * 2; }
+            for (int l = 0; l < nl; l++) { bias_off[l] = total_b; total_b += TC_NMAX * sizeof(float); }
+            std::vector<unsigned char> hb(total_b, 0);
+            auto put_w = [&](int l, int n, int k, float v) {
+                const __half hi = __float2half_rn(v);
+                const __half lo = __float2half_rn((v - __half2float(hi)) * 2048.0f);
+                const size_t o = umma::op_offset(n, k, Ks[l]);
+                memcpy(&hb[boff[l] + o], &hi, 2);
+                memcpy(&hb[boff[l] + (size_t)Ns[l] * Ks[l] * 2 + o], &lo, 2);
+            };
+            for (int t = 0; t < T; t++)
+                for (int c = 0; c < 3; c++)
+                    for (int f = 0; f < C; f++) put_w(0, f, t * 3 + c, masked_w[(t * 3 + c) * C + f]);
+            for (int l = 0; l < NH; l++)
+                for (int o = 0; o < C; o++)
+                    for (int i = 0; i < C; i++) put_w(1 + l, o, i, hidden_w[((size_t)l * C + o) * C + i]);
+            for (int mm = 0; mm < M; mm++)
+                for (int i = 0; i < C; i++) put_w(nl - 1, mm, i, out_w[(size_t)mm * C + i]);
+            auto put_b = [&](int l, const float* b, int count) { memcpy(&hb[bias_off[l]], b, count * sizeof(float)); };
+            put_b(0, masked_b, C);
+            for (int l = 0; l < NH; l++) put_b(1 + l, hidden_b + (size_t)l * C, C);
+            put_b(nl - 1, out_b, M);
+            if (cudaMalloc(&m->d_tc, total_b) == cudaSuccess &&
+                cudaMemcpy(m->d_tc, hb.data(), total_b, cudaMemcpyHostToDevice) == cudaSuccess) {
+                m->tcnet.nl = nl; m->tcnet.M = M; m->tcnet.K0 = TC;
+                for (int l = 0; l < nl; l++) {
+                    m->tcnet.blob[l] = m->d_tc + boff[l];
+                    m->tcnet.bias[l] = reinterpret_cast<const float*>(m->d_tc + bias_off[l]);
+                    m->tcnet.N[l] = Ns[l]; m->tcnet.K[l] = Ks[l];
+                }
+                m->tc_ok = true;
+            }
+        }
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { cudaFree(m->d_w); delete m; return fail(LPIC_E_CUDA, cudaGetErrorString(e)); }
     *out = m;
@@ -971,13 +1099,16 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_step_off); cudaFree(m->d_chunks); cudaFree(m->d_ring); cudaFree(m->d_flags);
     cudaFree(m->d_progress);
     cudaFree(m->d_rcR); cudaFree(m->d_rcW); cudaFree(m->d_rcP); cudaFree(m->d_rcC);
+    cudaFree(m->d_tc);
     delete m;
     return 0;
 }
 
 int lpic_model_set_precision(lpic_model_t* m, int precision) {
     if (!m) return fail(LPIC_E_ARG, "null model");
-    if (precision != LPIC_PREC_COMPAT) return fail(LPIC_E_UNSUPPORTED, "only LPIC_PREC_COMPAT is built in this version");
+    if (precision != LPIC_PREC_COMPAT && precision != LPIC_PREC_FAST) return fail(LPIC_E_ARG, "unknown precision");
+    if (precision == LPIC_PREC_FAST && !m->tc_ok)
+        return fail(LPIC_E_UNSUPPORTED, "FAST precision needs filters <= 128, 12*mixtures <= 128, kernel_half <= 3");
     m->precision = precision;
     return 0;
 }

@@ -252,15 +252,37 @@ class GpuModel:
 
 
 _MODELS: dict = {}
+_PRECISION = {"compat": _native.PREC_COMPAT, "fast": _native.PREC_FAST}
+_precision = "compat"
+
+
+def set_precision(name: str) -> None:
+    """Select the network arithmetic of every subsequent encode/decode.
+
+    "compat" (default): the reference's canonical float32 order -- raw
+    parameters bit-identical to the CPU reference, streams interchangeable
+    with it.  "fast": tcgen05 tensor-core GEMMs with the fp16x3 split (raw
+    within ~1e-5 relative); such streams round-trip on this library only and
+    must be decoded with precision "fast" too (the container does not record
+    it, exactly as it does not record the weights beyond their fingerprint).
+    """
+    global _precision
+    if name not in _PRECISION:
+        raise ValueError(f"precision must be one of {sorted(_PRECISION)}")
+    _precision = name
+
+
+def get_precision() -> str:
+    return _precision
 
 
 def gpu_model(w: Weights, cfg: ModelConfig) -> GpuModel:
     import torch
     _native.require_cuda()
-    key = (weight_fingerprint(w, cfg), cfg, torch.cuda.current_device())
+    key = (weight_fingerprint(w, cfg), cfg, torch.cuda.current_device(), _precision)
     m = _MODELS.get(key)
     if m is None:
-        m = GpuModel(w, cfg)
+        m = GpuModel(w, cfg, _PRECISION[_precision])
         _MODELS[key] = m
     return m
 

@@ -321,3 +321,37 @@ def test_gpu_true_symbol_probs_vs_oracle(P, oracle_mod):
         ref = oracle_mod.true_symbol_probs(raw, syms, rn, gn, K, dist)
         # float64 CDF differences: the GPU Phi and glibc erfc agree to ~1e-16 absolute
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-14), np.max(np.abs(got - ref))
+
+
+@pytest.mark.gpu
+def test_gpu_fast_precision_raw_and_roundtrip(P):
+    """LPIC_PREC_FAST: tcgen05 fp16x3 network.  Raw parameters within the
+    north-star budget of the compat (reference-exact) network; FAST streams
+    round-trip through the FAST decoder; bpsp within 0.5% of compat."""
+    from paper_2212_01185_b200 import synth
+    w, cfg = make_weights("ref", "kaiming", 0)
+    img = synth.synth_1f(0, 48, 40, beta=2.0, sigma=3.0)
+    tc = P.CodecTrace()
+    P.set_precision("compat")
+    try:
+        cc = P.encode(img, w, cfg, "wave", trace=tc)
+        P.set_precision("fast")
+        tf = P.CodecTrace()
+        cf = P.encode(img, w, cfg, "wave", trace=tf)
+        ref = tc.raw.astype(np.float64)
+        err = np.abs(tf.raw.astype(np.float64) - ref)
+        rel = err / np.maximum(np.abs(ref), 0.1)
+        assert rel.max() < 1e-4, rel.max()
+        assert np.array_equal(P.decode(cf, w, cfg), img)
+        td = P.CodecTrace()
+        P.decode(cf, w, cfg, trace=td)
+        assert np.array_equal(td.raw, tf.raw) and np.array_equal(td.cdfs, tf.cdfs)
+        assert abs(P.bpsp(cf) - P.bpsp(cc)) <= 0.005 * P.bpsp(cc)
+        # other model configs run FAST too (K = 2, C = 8 / 16, h = 1)
+        for name in ("tiny", "small", "h1"):
+            w2, cfg2 = make_weights(name, "glorot", 7)
+            im2 = synth.synth_1f(3, 20, 24)
+            c2 = P.encode(im2, w2, cfg2, "wave")
+            assert np.array_equal(P.decode(c2, w2, cfg2), im2)
+    finally:
+        P.set_precision("compat")
