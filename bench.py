@@ -270,6 +270,19 @@ def run_ours(args, cfgd):
         enc_ms, enc_launch = timed(enc_dev, args.steps)
     torch.cuda.synchronize()
     assert torch.equal(d_out, d_imgs), "decoder is not lossless"
+    # the encoder's network stage on its own (K1 in SURVEY 2.2): compat = CUDA
+    # cores in canonical fp32 order, fast = tcgen05 fp16x3 GEMMs
+    d_rawnet = torch.empty((n, N, 12 * cfg.mixtures), dtype=torch.float32, device=dev)
+
+    def net_dev():
+        _native.check(L.lpic_network_coding_order(m.handle, d_imgs.data_ptr(), n, H, W, int(mode),
+                                                   d_rawnet.data_ptr(), sp), "network")
+
+    for _ in range(2):
+        net_dev()
+    stream.synchronize()
+    net_ms, _ = timed(net_dev, args.steps)
+    del d_rawnet
     tot_dec = torch.tensor([sum(dec_ms)], dtype=torch.float64, device=dev)
     tot_enc = torch.tensor([sum(enc_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -346,6 +359,14 @@ def run_ours(args, cfgd):
                          "peak_kind": peak_kind,
                          "note": "model FLOPs (38,912/sub-pixel) per decode; the decoder is bound by the serial "
                                  "per-stream range-coder chain, see DESIGN.md"},
+            "encode_network": {
+                "kernel": "k_enc_net_tc (tcgen05)" if args.precision == "fast" else "k_enc_net (CUDA cores)",
+                "ms": sum(net_ms) / len(net_ms),
+                "model_tflops": 2.0 * 58368 * N * n / (sum(net_ms) / len(net_ms) / 1e3) / 1e12,
+                "frac_of_bf16_peak": 2.0 * 58368 * N * n / (sum(net_ms) / len(net_ms) / 1e3) / 1e12 / peaks["bf16_tflops"],
+                "note": "model FLOPs (58,368 MAC/px); the fp16x3 split issues 3 MMAs per product "
+                        "and pads K 36->48, N 36->48" if args.precision == "fast" else
+                        "model FLOPs; canonical fp32 order (no FMA) cannot use tensor cores"},
             "gpu_launches": dec_launch,
             "clocks": clk.summary(),
         }

@@ -117,6 +117,12 @@ int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, in
 int lpic_decode_batch(lpic_model_t* m, const uint8_t* h_payload, const int64_t* h_offs,
                       const int64_t* h_lens, int n, int H, int W, int mode, uint8_t* h_images,
                       int32_t* h_status, void* stream);
+/* The encoder's network stage alone (codec._raw_in_coding_order,
+ * codec.py:116-145, in the model's precision): d_images (n,H,W,3) u8 ->
+ * d_raw (n, H*W, 12K) f32 in coding order.  Used to time the network
+ * kernel (compat: CUDA cores; FAST: tcgen05) on its own. */
+int lpic_network_coding_order(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, float* d_raw,
+                              void* stream);
 /* codec.theoretical_bpsp (codec.py:255-274): -log2 of the unquantised
  * probability of every sub-pixel, in coding order: d_bits (n, H*W, 3) f64
  * (theoretical_bpsp = sum / (3HW)). */

@@ -1190,6 +1190,28 @@ int lpic_true_symbol_probs(const float* d_raw, int64_t N, int M, int K, int dist
     return 0;
 }
 
+int lpic_network_coding_order(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, float* d_raw,
+                              void* stream) {
+    if (int r = check_geom(m, n, H, W, mode)) return r;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lk(m->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int r = coding_order(m, H, W, mode, st)) return r;
+    if (int r = ensure(m->d_status, m->status_cap, (size_t)n)) return r;
+    CUDA_TRY(cudaMemsetAsync(m->d_status, 0, sizeof(int32_t) * n, st));
+    if (m->precision == LPIC_PREC_FAST) {
+        int r = LPIC_E_UNSUPPORTED;
+        if (m->h == 1) r = launch_enc_net_tc<1>(m, d_images, n, H, W, mode, d_raw, m->d_status, nullptr, st);
+        else if (m->h == 2) r = launch_enc_net_tc<2>(m, d_images, n, H, W, mode, d_raw, m->d_status, nullptr, st);
+        else if (m->h == 3) r = launch_enc_net_tc<3>(m, d_images, n, H, W, mode, d_raw, m->d_status, nullptr, st);
+        if (r) return r;
+    } else if (int r = dispatch<NetRun>(m->CP, m->h, m, d_images, n, H, W, mode, d_raw, m->d_status, st)) {
+        return r;
+    }
+    m->launches = 1;
+    return 0;
+}
+
 int lpic_theoretical_bits(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, double* d_bits,
                           void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
