@@ -49,6 +49,8 @@ struct ChainSmem {
     alignas(16) unsigned long long wq[CH_WARPS];  // per-warp fixed-point PMF sums
     alignas(16) int wm[CH_WARPS];                 // per-warp sums of m
     alignas(16) double wedge[CH_WARPS][KMAX];     // each warp's last upper-edge CDF value per component
+    float wedgeq[CH_WARPS][KMAX];                 // (FAST) last upper edge as (Q, above-zero)
+    int wedgep[CH_WARPS][KMAX];
 };
 
 // key order of the reference's deficit selection: larger remainder first,
@@ -93,7 +95,9 @@ __device__ __forceinline__ uint32_t digit_lanes(int d, const uint32_t (&inv)[5])
 // KU > 0: compile-time component count; KU == 0: runtime K (<= KMAX)
 // want_sym < 0: decoder -- find the symbol whose interval holds `target`;
 // want_sym >= 0: encoder -- return that symbol's (start, mass).
-template <int KU, bool BLUE>
+// F32: FAST-precision tables (float32 Phi/PMF/quantisation, lpic_cdf.cuh),
+// bin-for-bin identical to warp_pmf32 / warp_quantize32.
+template <int KU, bool BLUE, bool F32 = false>
 __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const double* __restrict__ inv,
                                             const float* __restrict__ mu0, const float* __restrict__ t1,
                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
@@ -106,6 +110,58 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     const int k0 = 2 * t;                                   // bins k0, k0 + 1
     CHP0;
 
+    double p0 = 0.0, p1 = 0.0;
+    if constexpr (F32) {
+    // ---- P (float32): Q = Phi(-|z|) and the sign at the upper edges of both bins
+    const float e0 = cc->edges32[k0 + 1], e1 = cc->edges32[k0 + 2];
+    float qa[KC], qb[KC];
+    bool pa[KC], pb[KC];
+#pragma unroll
+    for (int q = 0; q < KC; q++) {
+        if (KU == 0 && q >= K) break;
+        const float m32 = BLUE ? __fadd_rn(__fadd_rn(mu0[q], __fmul_rn(t1[q], rn)), __fmul_rn(t2[q], gn))
+                               : __fadd_rn(mu0[q], __fmul_rn(t1[q], rn));
+        const float iv = __double2float_rn(inv[q]);
+        const float z0 = __fmul_rn(__fsub_rn(e0, m32), iv), z1 = __fmul_rn(__fsub_rn(e1, m32), iv);
+        qa[q] = phiq32(z0, cc->phic32); pa[q] = z0 > 0.0f;
+        qb[q] = phiq32(z1, cc->phic32); pb[q] = z1 > 0.0f;
+        if (k0 + 1 == 255) { qb[q] = 0.0f; pb[q] = true; }             // +inf
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int q = 0; q < KC; q++) {
+            if (KU == 0 && q >= K) break;
+            cs->wedgeq[w][q] = qb[q]; cs->wedgep[w][q] = pb[q];
+        }
+    }
+    CHP(0);
+    chain_sync(bar);                                                                        // E
+    CHP(1);
+    float f0 = 0.0f, f1 = 0.0f;
+#pragma unroll
+    for (int q = 0; q < KC; q++) {
+        if (KU == 0 && q >= K) break;
+        float qp = __shfl_up_sync(0xffffffffu, qb[q], 1);
+        bool pp = __shfl_up_sync(0xffffffffu, (int)pb[q], 1) != 0;
+        if (lane == 0) {
+            if (w == 0) { qp = 0.0f; pp = false; }                           // -inf
+            else { qp = cs->wedgeq[w - 1][q]; pp = cs->wedgep[w - 1][q] != 0; }
+        }
+        const float d0 = bin_prob32(qp, pp, qa[q], pa[q]), d1 = bin_prob32(qa[q], pa[q], qb[q], pb[q]);
+        const float piq = __double2float_rn(pi[q]);
+        const float n0 = __fadd_rn(f0, __fmul_rn(piq, d0)), n1 = __fadd_rn(f1, __fmul_rn(piq, d1));
+        f0 = d0 > 0.0f ? n0 : f0;
+        f1 = d1 > 0.0f ? n1 : f1;
+    }
+    p0 = (double)f0; p1 = (double)f1;                  // exact; used only through fx_bin and the fp32 quantiser
+    {
+        const unsigned long long wsum = fx_warp_sum(fx_bin(p0) + fx_bin(p1));
+        if (lane == 0) cs->wq[w] = wsum;
+    }
+    CHP(2);
+    chain_sync(bar);                                                                        // T
+    CHP(3);
+    } else {
     // ---- P: CDF at the upper edges of both bins, every component
     const double e0 = cc->edges[k0 + 1], e1 = cc->edges[k0 + 2];
     double cur[2 * KC];
@@ -150,7 +206,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // E
     CHP(1);
     // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
-    double p0 = 0.0, p1 = 0.0;
+    p0 = 0.0; p1 = 0.0;
 #pragma unroll
     for (int q = 0; q < KC; q++) {
         if (KU == 0 && q >= K) break;
@@ -170,18 +226,31 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // T
     CHP(3);
 
+    }
     // ---- Q: floors, remainders, digits (kernels.py:272-285)
     {
         const ulonglong2 q01 = reinterpret_cast<const ulonglong2*>(cs->wq)[0];
         const ulonglong2 q23 = reinterpret_cast<const ulonglong2*>(cs->wq)[1];
-        const double scale = cdf_scale(fx_total((q01.x + q01.y) + (q23.x + q23.y)));
-        CHP(10);
-        const double v0 = __dmul_rn(p0, scale), v1 = __dmul_rn(p1, scale);
-        double f0 = floor(v0), f1 = floor(v1);
-        f0 = f0 > CDF_FLOOR ? CDF_FLOOR : f0;
-        f1 = f1 > CDF_FLOOR ? CDF_FLOOR : f1;
-        const int m0 = (int)f0 + 1, m1 = (int)f1 + 1;
-        const double fr0 = __dsub_rn(v0, f0), fr1 = __dsub_rn(v1, f1);     // == -(f - v) exactly
+        int m0, m1;
+        double fr0, fr1;
+        if constexpr (F32) {
+            const float scale = __fdiv_rn(CDF_FLOOR_F, __double2float_rn(fx_total((q01.x + q01.y) + (q23.x + q23.y))));
+            const float v0 = __fmul_rn((float)p0, scale), v1 = __fmul_rn((float)p1, scale);
+            float f0 = floorf(v0), f1 = floorf(v1);
+            f0 = f0 > CDF_FLOOR_F ? CDF_FLOOR_F : f0;
+            f1 = f1 > CDF_FLOOR_F ? CDF_FLOOR_F : f1;
+            m0 = (int)f0 + 1; m1 = (int)f1 + 1;
+            fr0 = (double)__fsub_rn(v0, f0); fr1 = (double)__fsub_rn(v1, f1);
+        } else {
+            const double scale = cdf_scale(fx_total((q01.x + q01.y) + (q23.x + q23.y)));
+            CHP(10);
+            const double v0 = __dmul_rn(p0, scale), v1 = __dmul_rn(p1, scale);
+            double f0 = floor(v0), f1 = floor(v1);
+            f0 = f0 > CDF_FLOOR ? CDF_FLOOR : f0;
+            f1 = f1 > CDF_FLOOR ? CDF_FLOOR : f1;
+            m0 = (int)f0 + 1; m1 = (int)f1 + 1;
+            fr0 = __dsub_rn(v0, f0); fr1 = __dsub_rn(v1, f1);     // == -(f - v) exactly
+        }
         const int d0 = min(__double2int_rz(__dmul_rn(fr0, 32.0)), 31);
         const int d1 = min(__double2int_rz(__dmul_rn(fr1, 32.0)), 31);
         reinterpret_cast<double2*>(cs->frac)[t] = make_double2(fr0, fr1);

@@ -40,6 +40,7 @@ struct DecParams {
     NetDev w;
     TcNetDev tc;                 // FAST precision network (lpic_net_tc.cuh)
     int fast;
+    int f32;                     // FAST float32 tables (fast && Gaussian)
     int S;                       // streams per cluster (chains per consumer CTA)
     int n;                       // streams in the launch
     int K, dist, H, W, mode, a;
@@ -276,7 +277,8 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         // red tables: warp w builds the tables of pixels w, w+8, ...
         for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
             uint32_t start[8], mass[8];
-            warp_table(rawbuf + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
+            if (P.f32) warp_table32(rawbuf + p * P.w.MP, K, 0, 0.0f, 0.0f, cc, start, mass);
+            else warp_table(rawbuf + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
             uint4 v;
             v.x = (start[0] & 0xFFFFu) | (start[1] << 16); v.y = (start[2] & 0xFFFFu) | (start[3] << 16);
@@ -308,7 +310,7 @@ struct ConsumerSmem {
     ChainSmem ch;
 };
 
-template <int KU, int NT>
+template <int KU, int NT, bool F32>
 __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * P.rec_bytes;
@@ -436,7 +438,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned
         int sg;
         uint32_t st, ms;
         target = dec.target(r);
-        chain_table<KU, false>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, target, sg,
+        chain_table<KU, false, F32>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, target, sg,
                                st, ms, trow ? trow + 257 : nullptr, -1, bar);
         dec.advance(r, st, ms);
         const float gn = cc->lut[sg];
@@ -444,7 +446,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned
         // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
         int sb;
         target = dec.target(r);
-        chain_table<KU, true>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, target, sb, st,
+        chain_table<KU, true, F32>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, target, sb, st,
                               ms, trow ? trow + 514 : nullptr, -1, bar);
         dec.advance(r, st, ms);
         if (dbg && ct == 0) dbg[8] = clock64();
@@ -468,9 +470,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) k_decode2(con
     extern __shared__ __align__(128) unsigned char smem[];
     const int img0 = (blockIdx.x >> 1) * P.S;
     if (cluster_rank() == 0) {
-        if (P.K == 3) dec_consumer<3, NT>(P, img0, smem);
-        else if (P.K == 2) dec_consumer<2, NT>(P, img0, smem);
-        else dec_consumer<0, NT>(P, img0, smem);
+        if (P.f32) {
+            if (P.K == 3) dec_consumer<3, NT, true>(P, img0, smem);
+            else if (P.K == 2) dec_consumer<2, NT, true>(P, img0, smem);
+            else dec_consumer<0, NT, true>(P, img0, smem);
+        } else {
+            if (P.K == 3) dec_consumer<3, NT, false>(P, img0, smem);
+            else if (P.K == 2) dec_consumer<2, NT, false>(P, img0, smem);
+            else dec_consumer<0, NT, false>(P, img0, smem);
+        }
     } else {
         dec_producer<CP, HH>(P, img0, smem);
     }

@@ -188,7 +188,7 @@ constexpr int TAB_WARPS = 8;
 __global__ void __launch_bounds__(TAB_WARPS * 32)
 k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
-             int32_t* trace_cdf) {
+             int32_t* trace_cdf, int f32) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ WarpCdfScratch sc[TAB_WARPS];
     __shared__ float rbuf[TAB_WARPS][12 * KMAX];
@@ -210,7 +210,8 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
 #pragma unroll 1
             for (int ch = 0; ch < 3; ch++) {
                 uint32_t start[8], mass[8];
-                warp_table(rbuf[wid], K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, sc + wid, start, mass);
+                if (f32) warp_table32(rbuf[wid], K, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, start, mass);
+                else warp_table(rbuf[wid], K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, sc + wid, start, mass);
                 const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
                 if (lane == (sym >> 3)) {
                     uint32_t st = 0, ms = 1;
@@ -232,9 +233,15 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
 #pragma unroll 1
         for (int ch = 0; ch < 3; ch++) {
             uint32_t start[8], mass[8];
-            double pmf[8];
-            warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, ch * K);
-            warp_quantize(pmf, sc + wid, start, mass);
+            if (f32) {                                      // FAST float32 tables (Gaussian)
+                float pmf[8];
+                warp_pmf32(__double2float_rn(pi_l), (float)mu_l, __double2float_rn(inv_l), K, &cc, pmf, ch * K);
+                warp_quantize32(pmf, start, mass);
+            } else {
+                double pmf[8];
+                warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, ch * K);
+                warp_quantize(pmf, sc + wid, start, mass);
+            }
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
             if (lane == (sym >> 3)) {
                 uint32_t st = 0, ms = 1;
@@ -809,7 +816,8 @@ template <int CP, int HH> struct EncodeRun {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
         const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
         const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
-        k_enc_tables<<<g2, TAB_WARPS * 32, 0, st>>>(raw, m->M, m->K, m->dist, d_images, W, m->d_order, N, total, sw, tc);
+        k_enc_tables<<<g2, TAB_WARPS * 32, 0, st>>>(raw, m->M, m->K, m->dist, d_images, W, m->d_order, N, total, sw, tc,
+                                                    (m->precision == LPIC_PREC_FAST && m->dist == 0) ? 1 : 0);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -913,6 +921,7 @@ template <int CP, int HH> struct DecodeRun {
         P.dbg = m->d_dbg;
         P.S = S; P.n = n;
         P.fast = fast ? 1 : 0; P.tc = m->tcnet;
+        P.f32 = (fast && m->dist == 0) ? 1 : 0;
         // the k_decode2 instantiations live in lpic_decode_cp*.cu (compiled in parallel)
         cudaError_t e = launch_decode2(CP, HH, S, n, smem, st, P);
         if (e != cudaSuccess) return fail(LPIC_E_CUDA, std::string("k_decode2: ") + cudaGetErrorString(e));

@@ -32,6 +32,7 @@ __device__ float urand(uint32_t& s, float lo, float hi) { s = hash32(s + 0x9e377
 
 // one CTA per case: warp 0 builds the reference table with warp_table, then
 // the 4 chain warps run chain_table on the same mixture record
+template <bool F32>
 __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, float scale, int* bad, int32_t* rows) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ __align__(16) CSM cs;
@@ -64,7 +65,8 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
         __syncthreads();
         if (threadIdx.x < 32) {
             uint32_t st[8], ms[8];
-            warp_table(raw, K, dist, ch, rn, ch == 2 ? gn : 0.0f, &cc, &ws, st, ms);
+            if (F32) warp_table32(raw, K, ch, rn, ch == 2 ? gn : 0.0f, &cc, st, ms);
+            else warp_table(raw, K, dist, ch, rn, ch == 2 ? gn : 0.0f, &cc, &ws, st, ms);
             for (int q = 0; q < 8; q++) ref[8 * threadIdx.x + q] = (int32_t)st[q];
             if (threadIdx.x == 31) ref[256] = (int32_t)(st[7] + ms[7]);
         }
@@ -75,14 +77,14 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
             const uint32_t target = s3 & 0xFFFFu;
             int sym; uint32_t start, mass;
             if (K == 3) {
-                if (ch == 1) CT<3, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else CT<3, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<3, false, F32>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<3, true, F32>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             } else if (K == 2) {
-                if (ch == 1) CT<2, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else CT<2, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<2, false, F32>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<2, true, F32>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             } else {
-                if (ch == 1) CT<0, false>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
-                else CT<0, true>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
+                if (ch == 1) CT<0, false, F32>(pi, inv, mu0, ta, nullptr, rn, 0.0f, K, dist, &cc, &cs, target, sym, start, mass, got);
+                else CT<0, true, F32>(pi, inv, mu0, ta, tb, rn, gn, K, dist, &cc, &cs, target, sym, start, mass, got);
             }
             __syncthreads();
             // expected symbol from the reference table
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
     }
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(NTH) k_time(int tables, long long* out) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ __align__(16) CSM cs;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(NTH) k_time(int tables, long long* out) {
     for (int it = 0; it < tables; it++) {
         const float rn = -1.0f + 0.001f * (it & 1023);
         int sym; uint32_t st, ms;
-        CT<3, true>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
+        CT<3, true, F32>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
         acc += st + ms;
         target = (target * 2654435761u + st) & 0xFFFFu;     // dependency on the previous result
     }
@@ -140,12 +143,13 @@ int main() {
     const int Ks[4] = {3, 2, 5, 1};
     const float scales[3] = {1.0f, 3.0f, 8.0f};
     int total_bad = 0;
-    for (int dist = 0; dist < 2; dist++)
+    for (int dist = 0; dist < 3; dist++)                 // 2: FAST float32 tables (Gaussian)
         for (int ki = 0; ki < 4; ki++)
             for (int si = 0; si < 3; si++) {
                 cudaMemset(bad, 0, 8);
                 const int n = 4000;
-                k_check<<<296, NTH>>>(n, Ks[ki], dist, scales[si], bad, rows);
+                if (dist == 2) k_check<true><<<296, NTH>>>(n, Ks[ki], 0, scales[si], bad, rows);
+                else k_check<false><<<296, NTH>>>(n, Ks[ki], dist, scales[si], bad, rows);
                 int hb[2]; cudaMemcpy(hb, bad, 8, cudaMemcpyDeviceToHost);
                 printf("check K=%d dist=%d scale=%.0f: %d / %d mismatches\n", Ks[ki], dist, scales[si], hb[0], 3 * n);
                 total_bad += hb[0];
@@ -157,8 +161,13 @@ int main() {
                         if (h[k] != h[257 + k]) { printf("  k=%d ref %d got %d\n", k, h[k], h[257 + k]); shown++; }
                 }
             }
-    k_time<<<1, NTH>>>(20, d); cudaDeviceSynchronize();
-    k_time<<<1, NTH>>>(4000, d);
+    k_time<false><<<1, NTH>>>(20, d); cudaDeviceSynchronize();
+    k_time<true><<<1, NTH>>>(4000, d);
+    {
+        long long h32[2]; cudaMemcpy(h32, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 FAST(f32): %lld cycles per table\n", h32[0]);
+    }
+    k_time<false><<<1, NTH>>>(4000, d);
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("chain_table K=3: %lld cycles per table (%s)\n", h[0], cudaGetErrorString(cudaGetLastError()));
 #ifdef PROF
