@@ -355,3 +355,23 @@ def test_gpu_fast_precision_raw_and_roundtrip(P):
             assert np.array_equal(P.decode(c2, w2, cfg2), im2)
     finally:
         P.set_precision("compat")
+
+
+@pytest.mark.gpu
+def test_gpu_two_streams_per_cluster(P, oracle_mod):
+    """Throughput mode (two streams per cluster, chosen automatically for many
+    streams) forced on a small odd batch: lossless and byte-identical to the
+    one-stream-per-cluster decode of the same reference-exact payloads."""
+    from paper_2212_01185_b200 import synth
+    w, cfg = make_weights("small", "glorot", 7)
+    imgs = [synth.synth_1f(40 + k, 18, 23) for k in range(5)]
+    conts = P.encode_batch(imgs, w, cfg, "wave")
+    os.environ["LPIC_DEC_STREAMS_PER_CLUSTER"] = "2"
+    try:
+        outs = P.decode_batch(conts, w, cfg)
+    finally:
+        del os.environ["LPIC_DEC_STREAMS_PER_CLUSTER"]
+    for a, b in zip(outs, imgs):
+        assert np.array_equal(a, b)
+    ow = oracle_weights(oracle_mod, w, cfg)
+    assert conts[0].payload == oracle_mod.encode(ow, imgs[0], "wave")
