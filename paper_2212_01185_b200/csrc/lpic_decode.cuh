@@ -158,18 +158,17 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // ---------------------------------------------------------------------------
 // producer
 // ---------------------------------------------------------------------------
+__host__ __device__ constexpr size_t dec_fbase_off() {
+    return (sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127;
+}
 template <int CP, int HH>
 __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
     WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
-    float* fbase = reinterpret_cast<float*>(smem + sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch));
+    float* fbase = reinterpret_cast<float*>(smem + dec_fbase_off());
     constexpr int TC = Taps<HH>::TC;
     NetTileBufs nb;
-    nb.act0 = fbase;
-    nb.act1 = nb.act0 + (CP > TC ? CP : TC) * NT_TP;
-    nb.wbuf = nb.act1 + CP * NT_TP;
-    nb.raw = nb.wbuf + ((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * P.w.MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
-                                                                           : CP * P.w.MT);
+    net_tile_carve(fbase, CP, TC, P.w.MT, P.w.MP, nb);
     __shared__ long long s_need;
     // FAST precision: the tensor-core tile state and a raw buffer replace the fp32 tile buffers
     const size_t tc_off = (sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127;
@@ -178,6 +177,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     uint32_t mcnt = 0;
     load_consts(cc);
     if (P.fast && threadIdx.x < 128) tc_init(tcs);
+    if (!P.fast && threadIdx.x == 0) net_tile_init(nb);
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
@@ -193,6 +193,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         const int c = cs_ / P.S;
         img = img0 + cs_ % P.S;
         if (img >= P.n) continue;
+        if (!P.fast) net_tile_prefetch(P.w, nb);          // layer 0 lands during the wait + gather
         const uint8_t* im = P.images + (int64_t)img * N * 3;
         uint8_t* ring = P.ring + (int64_t)img * P.ring_size * P.rec_bytes;
         uint32_t* flags = P.flags + (int64_t)img * P.ring_size;

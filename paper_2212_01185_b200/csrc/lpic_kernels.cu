@@ -89,11 +89,11 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
     __shared__ float lut[256];
     float* fb = reinterpret_cast<float*>(smem);
     NetTileBufs nb;
-    nb.act0 = fb;
-    nb.act1 = nb.act0 + (CP > TC ? CP : TC) * NT_TP;
-    nb.wbuf = nb.act1 + CP * NT_TP;
-    nb.raw = nb.wbuf + ((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * w.MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
-                                                                         : CP * w.MT);
+    net_tile_carve(fb, CP, TC, w.MT, w.MP, nb);
+    if (threadIdx.x == 0) {
+        net_tile_init(nb);
+        net_tile_load(w, nb, 0, 0);                       // layer 0 streams in during the gather
+    }
     for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
     __syncthreads();
     const int img = blockIdx.y, tid = threadIdx.x;
@@ -878,7 +878,7 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
 size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S, bool fast) {
     const size_t prod = fast ? ((sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127) +
                                    sizeof(TcSmem) + (size_t)NT_TP * MP * 4
-                             : sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + net_tile_floats(CP, TC, MT, MP) * 4;
+                             : dec_fbase_off() + net_tile_floats(CP, TC, MT, MP) * 4;
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
     const size_t cons = ((sizeof(CdfConsts) + 127) & ~(size_t)127) + (size_t)S * grp;
     return prod > cons ? prod : cons;

@@ -131,15 +131,59 @@ constexpr int NT_TP = 64;
 struct NetTileBufs {
     float* act0;     // [max(CP, TC)][NT_TP]; holds the gathered taps on entry
     float* act1;     // [CP][NT_TP]
-    float* wbuf;     // max(TC*CP, CP*CP, CP*MT) floats
+    float* wbuf;     // layer weight double buffer: 2 x wstride floats
+    int wstride;     // net_wbuf_floats = max(TC*CP, CP*CP, CP*MT)
     float* raw;      // [NT_TP][MP] output
+    uint64_t* wbar;  // 2 mbarriers: weights of buffer b landed
+    uint32_t wuse0, wuse1;   // completed waits per buffer (every thread keeps the same count)
 };
 
+__host__ __device__ constexpr size_t net_wbuf_floats(int CP, int TC, int MT) {
+    return (size_t)((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
+                                                                       : CP * MT);
+}
 __host__ __device__ constexpr size_t net_tile_floats(int CP, int TC, int MT, int MP) {
-    return (size_t)(CP > TC ? CP : TC) * NT_TP + (size_t)CP * NT_TP +
-           (size_t)((TC * CP > CP * CP ? TC * CP : CP * CP) > CP * MT ? (TC * CP > CP * CP ? TC * CP : CP * CP)
-                                                                       : CP * MT) +
-           (size_t)NT_TP * MP;
+    return (size_t)(CP > TC ? CP : TC) * NT_TP + (size_t)CP * NT_TP + 2 * net_wbuf_floats(CP, TC, MT) +
+           (size_t)NT_TP * MP + 8;   // + 2 mbarriers (4 floats each, 16-byte aligned)
+}
+// carve the buffers out of `base` (16-byte aligned, net_tile_floats floats)
+__device__ __forceinline__ void net_tile_carve(float* base, int CP, int TC, int MT, int MP, NetTileBufs& nb) {
+    nb.act0 = base;
+    nb.act1 = nb.act0 + (CP > TC ? CP : TC) * NT_TP;
+    nb.wbuf = nb.act1 + CP * NT_TP;
+    nb.wstride = (int)net_wbuf_floats(CP, TC, MT);
+    nb.raw = nb.wbuf + 2 * nb.wstride;
+    nb.wbar = reinterpret_cast<uint64_t*>(nb.raw + NT_TP * MP);   // 16-byte aligned (NT_TP * MP % 4 == 0)
+    nb.wuse0 = nb.wuse1 = 0;
+}
+__device__ __forceinline__ uint32_t nt_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// thread 0, once per CTA (callers fence + __syncthreads afterwards)
+__device__ __forceinline__ void net_tile_init(const NetTileBufs& nb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(nt_smem(&nb.wbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(nt_smem(&nb.wbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// thread 0: bulk-copy layer l's input-major weights into buffer b
+__device__ __forceinline__ void net_tile_load(const NetDev& w, const NetTileBufs& nb, int l, int b) {
+    const int nl = w.NH + 2;
+    const float* src = l == 0 ? w.mwI : (l < nl - 1 ? w.hwI + (int64_t)(l - 1) * w.CP * w.CP : w.owI);
+    const uint32_t bytes = (uint32_t)(4 * (l == 0 ? w.TC * w.CP : (l < nl - 1 ? w.CP * w.CP : w.CP * w.MT)));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(nt_smem(&nb.wbar[b])), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(nt_smem(nb.wbuf + (b ? nb.wstride : 0))), "l"(src), "r"(bytes), "r"(nt_smem(&nb.wbar[b])) : "memory");
+}
+// thread 0: request the first layer of the next tile (buffer 0 must be idle)
+__device__ __forceinline__ void net_tile_prefetch(const NetDev& w, const NetTileBufs& nb) {
+    if (threadIdx.x == 0) net_tile_load(w, nb, 0, 0);
+}
+__device__ __forceinline__ void net_tile_wait(NetTileBufs& nb, int b) {
+    const uint32_t parity = (b ? nb.wuse1 : nb.wuse0) & 1u;
+    if (b) nb.wuse1++; else nb.wuse0++;
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(nt_smem(&nb.wbar[b])), "r"(parity) : "memory");
+    }
 }
 
 __device__ __forceinline__ void tile_copy(float* dst, const float* __restrict__ src, int n) {
@@ -168,7 +212,9 @@ __device__ __forceinline__ void load_w(const float* p, float (&wv)[F]) {
     }
 }
 
-// acc[p][f] = sum_{i<KD} W[i][og*F+f] * in[i][4pg+p], i ascending
+// acc[p][f] = sum_{i<KD} W[i][og*F+f] * in[i][4pg+p], i ascending.  The
+// operands of row i+1 are loaded while row i is multiplied (register double
+// buffer), so the shared-memory latency hides behind the 8F products.
 template <int KD, int F>
 __device__ __forceinline__ void tile_layer(const float* in, const float* W, int nout, int og, int pg,
                                            float (&acc)[4][F]) {
@@ -176,17 +222,42 @@ __device__ __forceinline__ void tile_layer(const float* in, const float* W, int 
     for (int p = 0; p < 4; p++)
 #pragma unroll
         for (int f = 0; f < F; f++) acc[p][f] = 0.0f;
-#pragma unroll 4
+    const float* ap = in + 4 * pg;
+    const float* wp = W + og * F;
+    float4 an = *reinterpret_cast<const float4*>(ap);
+    float wn[F];
+    load_w<F>(wp, wn);
+#pragma unroll 2
     for (int i = 0; i < KD; i++) {
-        const float4 a = *reinterpret_cast<const float4*>(in + i * NT_TP + 4 * pg);
+        const float4 a = an;
         float wv[F];
-        load_w<F>(W + i * nout + og * F, wv);
+#pragma unroll
+        for (int f = 0; f < F; f++) wv[f] = wn[f];
+        const int inext = i + 1 < KD ? i + 1 : i;       // the last row reloads itself (no branch)
+        an = *reinterpret_cast<const float4*>(ap + inext * NT_TP);
+        load_w<F>(wp + inext * nout, wn);
 #pragma unroll
         for (int f = 0; f < F; f++) {
             acc[0][f] = __fadd_rn(acc[0][f], __fmul_rn(wv[f], a.x));
             acc[1][f] = __fadd_rn(acc[1][f], __fmul_rn(wv[f], a.y));
             acc[2][f] = __fadd_rn(acc[2][f], __fmul_rn(wv[f], a.z));
             acc[3][f] = __fadd_rn(acc[3][f], __fmul_rn(wv[f], a.w));
+        }
+    }
+}
+
+// output layer with FO outputs per thread known at compile time
+template <int CP, int FO>
+__device__ __forceinline__ void tile_out(const NetDev& w, const float* in, const float* wo, int og, int pg, float* raw) {
+    float acc[4][FO];
+    tile_layer<CP, FO>(in, wo, w.MT, og, pg, acc);
+#pragma unroll
+    for (int f = 0; f < FO; f++) {
+        const int m = og * FO + f;
+        if (m < w.M) {
+            const float bb = __ldg(w.ob + m);
+#pragma unroll
+            for (int p = 0; p < 4; p++) raw[(4 * pg + p) * w.MP + m] = __fadd_rn(acc[p][f], bb);
         }
     }
 }
@@ -204,16 +275,20 @@ __device__ __forceinline__ void tile_store_act(const float (&acc)[4][F], const f
     }
 }
 
-// Network of one tile.  On entry b.act0 holds the taps as [tc][p]; on exit
-// b.raw[p*MP + m] holds the raw parameters.  Five __syncthreads.
+// Network of one tile.  On entry b.act0 holds the taps as [tc][p] and layer
+// 0's weights were requested (net_tile_prefetch); on exit b.raw[p*MP + m]
+// holds the raw parameters.  Layer l+1's weights stream into the other
+// buffer (cp.async.bulk) while layer l computes.
 template <int CP, int TC>
-__device__ void net_tile(const NetDev& w, const NetTileBufs& b) {
+__device__ void net_tile(const NetDev& w, NetTileBufs& b) {
     constexpr int F = CP / 16;
     const int t = threadIdx.x, pg = t & 15, og = t >> 4;
     const bool worker = t < NT_THREADS;                  // extra warps only join the barriers
+    const int nl = w.NH + 2;
     float acc[4][F];
-    tile_copy(b.wbuf, w.mwI, TC * CP);                   // masked layer (kernels.py:98-113)
-    __syncthreads();
+    // masked layer (kernels.py:98-113)
+    net_tile_wait(b, 0);
+    if (t == 0) net_tile_load(w, b, 1, 1);
     if (worker) {
         tile_layer<TC, F>(b.act0, b.wbuf, CP, og, pg, acc);
         tile_store_act<F>(acc, w.mb, og, pg, b.act1);
@@ -222,27 +297,36 @@ __device__ void net_tile(const NetDev& w, const NetTileBufs& b) {
     float* in = b.act1;
     float* out = b.act0;
     for (int l = 0; l < w.NH; l++) {                     // hidden 1x1 layers (kernels.py:69-80)
-        tile_copy(b.wbuf, w.hwI + (int64_t)l * CP * CP, CP * CP);
-        __syncthreads();
+        const int L = l + 1, buf = L & 1;
+        net_tile_wait(b, buf);
+        if (t == 0 && L + 1 < nl) net_tile_load(w, b, L + 1, buf ^ 1);
         if (worker) {
-            tile_layer<CP, F>(in, b.wbuf, CP, og, pg, acc);
+            tile_layer<CP, F>(in, b.wbuf + (buf ? b.wstride : 0), CP, og, pg, acc);
             tile_store_act<F>(acc, w.hb + l * CP, og, pg, out);
         }
         __syncthreads();
         float* tmp = in; in = out; out = tmp;
     }
-    tile_copy(b.wbuf, w.owI, CP * w.MT);                  // output layer (kernels.py:81-85)
-    __syncthreads();
+    const int ob = (nl - 1) & 1;                         // output layer (kernels.py:81-85)
+    net_tile_wait(b, ob);
+    const float* wo = b.wbuf + (ob ? b.wstride : 0);
     const int FO = worker ? w.MT / 16 : 0;                // outputs per thread (<= 12)
+    if (FO == 3) {                                        // K = 3, 4 (the reference default)
+        tile_out<CP, 3>(w, in, wo, og, pg, b.raw);
+    } else if (FO == 2) {
+        tile_out<CP, 2>(w, in, wo, og, pg, b.raw);
+    } else if (FO == 4) {
+        tile_out<CP, 4>(w, in, wo, og, pg, b.raw);
+    } else if (FO > 0) {
     float oacc[4][12];
 #pragma unroll
     for (int p = 0; p < 4; p++)
 #pragma unroll
         for (int f = 0; f < 12; f++) oacc[p][f] = 0.0f;
 #pragma unroll 2
-    for (int i = 0; i < (worker ? CP : 0); i++) {
+    for (int i = 0; i < CP; i++) {
         const float4 a = *reinterpret_cast<const float4*>(in + i * NT_TP + 4 * pg);
-        const float* wr = b.wbuf + i * w.MT + og * FO;
+        const float* wr = wo + i * w.MT + og * FO;
 #pragma unroll
         for (int f = 0; f < 12; f++) {
             if (f < FO) {
@@ -262,6 +346,7 @@ __device__ void net_tile(const NetDev& w, const NetTileBufs& b) {
 #pragma unroll
             for (int p = 0; p < 4; p++) b.raw[(4 * pg + p) * w.MP + m] = __fadd_rn(oacc[p][f], bb);
         }
+    }
     }
     __syncthreads();
 }
