@@ -159,19 +159,19 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // producer
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr size_t dec_fbase_off() {
-    return (sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127;
+    return (sizeof(CdfConsts) + 127) & ~(size_t)127;
 }
 template <int CP, int HH>
 __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
-    WarpCdfScratch* sc = reinterpret_cast<WarpCdfScratch*>(smem + sizeof(CdfConsts));
+
     float* fbase = reinterpret_cast<float*>(smem + dec_fbase_off());
     constexpr int TC = Taps<HH>::TC;
     NetTileBufs nb;
     net_tile_carve(fbase, CP, TC, P.w.MT, P.w.MP, nb);
     __shared__ long long s_need;
     // FAST precision: the tensor-core tile state and a raw buffer replace the fp32 tile buffers
-    const size_t tc_off = (sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127;
+    const size_t tc_off = dec_fbase_off();
     TcSmem* tcs = reinterpret_cast<TcSmem*>(smem + tc_off);
     float* fraw = reinterpret_cast<float*>(smem + tc_off + sizeof(TcSmem));
     uint32_t mcnt = 0;
@@ -183,6 +183,9 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     umma::fence_after();
     if (P.fast && threadIdx.x < 128) tc_prefetch(tcs, P.tc);
     float* rawbuf = P.fast ? fraw : nb.raw;
+    // the red tables' selection histograms (8 warps x 1 KB) live in a buffer
+    // that is idle between the network and the next chunk's gather
+    WarpCdfScratch* sc = P.fast ? reinterpret_cast<WarpCdfScratch*>(tcs->a_lo) : reinterpret_cast<WarpCdfScratch*>(nb.act0);
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int K = P.K;
     const int64_t N = P.N;
@@ -278,7 +281,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         // red tables: warp w builds the tables of pixels w, w+8, ...
         for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
             uint32_t start[8], mass[8];
-            if (P.f32) warp_table32(rawbuf + p * P.w.MP, K, 0, 0.0f, 0.0f, cc, start, mass);
+            if (P.f32) warp_table32(rawbuf + p * P.w.MP, K, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             else warp_table(rawbuf + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
             uint4 v;

@@ -184,11 +184,17 @@ k_enc_net_tc(const __grid_constant__ TcNetDev w, const uint8_t* __restrict__ ima
 // encoder, stage 2: three quantised CDF tables per pixel (warp builder) and
 // the coded symbol's (start, width) in coding order (codec.py:168-182)
 // ---------------------------------------------------------------------------
+// VAR: 0 float64 Gaussian, 1 float64 logistic, 2 FAST float32 Gaussian; BIG:
+// 3K > 32 (one channel's mixture at a time).  One variant per kernel keeps
+// the code within the instruction caches.
 constexpr int TAB_WARPS = 8;
+template <int VAR, bool BIG>
 __global__ void __launch_bounds__(TAB_WARPS * 32)
-k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
+k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
-             int32_t* trace_cdf, int f32) {
+             int32_t* trace_cdf) {
+    constexpr bool f32 = VAR == 2;
+    constexpr int dist = VAR == 1 ? 1 : 0;
     __shared__ __align__(16) CdfConsts cc;
     __shared__ WarpCdfScratch sc[TAB_WARPS];
     __shared__ float rbuf[TAB_WARPS][12 * KMAX];
@@ -206,11 +212,11 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
         // mixture parameters of all three channels at once: lane ch*K + i
         // holds component i of channel ch (kernels.py:212-247)
         double pi_l = 0.0, mu_l = 0.0, inv_l = 1.0;
-        if (3 * K > 32) {                                  // (K > 10: one channel at a time)
+        if constexpr (BIG) {                               // (K > 10: one channel at a time)
 #pragma unroll 1
             for (int ch = 0; ch < 3; ch++) {
                 uint32_t start[8], mass[8];
-                if (f32) warp_table32(rbuf[wid], K, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, start, mass);
+                if constexpr (f32) warp_table32(rbuf[wid], K, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, sc + wid, start, mass);
                 else warp_table(rbuf[wid], K, dist, ch, ch >= 1 ? rn : 0.0f, ch == 2 ? gn : 0.0f, &cc, sc + wid, start, mass);
                 const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
                 if (lane == (sym >> 3)) {
@@ -223,7 +229,7 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
             }
             __syncwarp();
             continue;
-        }
+        } else {
         if (lane < 3 * K) {
             const int ch = lane / K, i = lane - ch * K;
             pi_l = mix_pi(rbuf[wid], K, ch, i);
@@ -233,13 +239,13 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
 #pragma unroll 1
         for (int ch = 0; ch < 3; ch++) {
             uint32_t start[8], mass[8];
-            if (f32) {                                      // FAST float32 tables (Gaussian)
+            if constexpr (f32) {                            // FAST float32 tables (Gaussian)
                 float pmf[8];
                 warp_pmf32(__double2float_rn(pi_l), (float)mu_l, __double2float_rn(inv_l), K, &cc, pmf, ch * K);
-                warp_quantize32(pmf, start, mass);
+                warp_quantize32(pmf, sc + wid, start, mass);
             } else {
                 double pmf[8];
-                warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, ch * K);
+                warp_pmf_t<dist>(pi_l, mu_l, inv_l, K, &cc, pmf, ch * K);
                 warp_quantize(pmf, sc + wid, start, mass);
             }
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
@@ -252,7 +258,22 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, int dist, const uint8_
             if (trace_cdf) store_cdf_row(trace_cdf + (g * 3 + ch) * 257, start, mass);
         }
         __syncwarp();
+        }
     }
+}
+
+template <int VAR>
+void launch_enc_tables_v(bool big, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
+                         const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc, cudaStream_t st) {
+    if (big) k_enc_tables<VAR, true><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc);
+    else k_enc_tables<VAR, false><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc);
+}
+void launch_enc_tables(int var, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
+                       const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc, cudaStream_t st) {
+    const bool big = 3 * K > 32;
+    if (var == 2) launch_enc_tables_v<2>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
+    else if (var == 1) launch_enc_tables_v<1>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
+    else launch_enc_tables_v<0>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -749,7 +770,6 @@ int set_smem(Kern k, size_t bytes) {
     return 0;
 }
 
-size_t table_smem() { return sizeof(CdfConsts) + 4 * sizeof(WarpCdfScratch); }
 
 int coding_order(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
     if (m->d_order && m->ord_H == H && m->ord_W == W && m->ord_mode == mode) return 0;
@@ -816,8 +836,8 @@ template <int CP, int HH> struct EncodeRun {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
         const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
         const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
-        k_enc_tables<<<g2, TAB_WARPS * 32, 0, st>>>(raw, m->M, m->K, m->dist, d_images, W, m->d_order, N, total, sw, tc,
-                                                    (m->precision == LPIC_PREC_FAST && m->dist == 0) ? 1 : 0);
+        launch_enc_tables((m->precision == LPIC_PREC_FAST && m->dist == 0) ? 2 : m->dist, g2, raw, m->M, m->K, d_images,
+                          W, m->d_order, N, total, sw, tc, st);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -876,7 +896,7 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
 }
 
 size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S, bool fast) {
-    const size_t prod = fast ? ((sizeof(CdfConsts) + 8 * sizeof(WarpCdfScratch) + 127) & ~(size_t)127) +
+    const size_t prod = fast ? dec_fbase_off() +
                                    sizeof(TcSmem) + (size_t)NT_TP * MP * 4
                              : dec_fbase_off() + net_tile_floats(CP, TC, MT, MP) * 4;
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;

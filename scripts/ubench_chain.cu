@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
         __syncthreads();
         if (threadIdx.x < 32) {
             uint32_t st[8], ms[8];
-            if (F32) warp_table32(raw, K, ch, rn, ch == 2 ? gn : 0.0f, &cc, st, ms);
+            if (F32) warp_table32(raw, K, ch, rn, ch == 2 ? gn : 0.0f, &cc, &ws, st, ms);
             else warp_table(raw, K, dist, ch, rn, ch == 2 ? gn : 0.0f, &cc, &ws, st, ms);
             for (int q = 0; q < 8; q++) ref[8 * threadIdx.x + q] = (int32_t)st[q];
             if (threadIdx.x == 31) ref[256] = (int32_t)(st[7] + ms[7]);
