@@ -46,6 +46,7 @@ typedef struct lpic_model lpic_model_t;
 #define LPIC_S_NONFINITE 1  /* codec.py:165-166  LpicError("network produced non-finite parameters") */
 #define LPIC_S_CORRUPT 2    /* coder.py:94-95    CorruptStreamError */
 #define LPIC_S_CAPACITY 4   /* output buffer too small */
+#define LPIC_S_INTERNAL 8   /* a device-side pipeline stage never received its input (bounded wait expired) */
 
 #define LPIC_PREC_COMPAT 0
 #define LPIC_PREC_FAST 1

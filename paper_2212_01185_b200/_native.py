@@ -12,7 +12,7 @@ import os
 from .errors import LpicError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblpic_b200.so")
+LIB_PATH = os.environ.get("LPIC_LIB", os.path.join(_HERE, "liblpic_b200.so"))   # (override: A/B builds)
 
 LPIC_OK = 0
 LPIC_E_ARG = -1
@@ -22,6 +22,7 @@ LPIC_E_NOMEM = -4
 LPIC_S_NONFINITE = 1
 LPIC_S_CORRUPT = 2
 LPIC_S_CAPACITY = 4
+LPIC_S_INTERNAL = 8
 PREC_COMPAT = 0
 PREC_FAST = 1
 

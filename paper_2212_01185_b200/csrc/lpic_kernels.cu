@@ -188,11 +188,12 @@ k_enc_net_tc(const __grid_constant__ TcNetDev w, const uint8_t* __restrict__ ima
 // 3K > 32 (one channel's mixture at a time).  One variant per kernel keeps
 // the code within the instruction caches.
 constexpr int TAB_WARPS = 8;
+constexpr int TAB_BATCH = 4;
 template <int VAR, bool BIG>
 __global__ void __launch_bounds__(TAB_WARPS * 32)
 k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
-             int32_t* trace_cdf) {
+             int32_t* trace_cdf, unsigned long long* __restrict__ ctr) {
     constexpr bool f32 = VAR == 2;
     constexpr int dist = VAR == 1 ? 1 : 0;
     __shared__ __align__(16) CdfConsts cc;
@@ -201,8 +202,25 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
     load_consts(&cc);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t g = (int64_t)blockIdx.x * TAB_WARPS + wid; g < total; g += (int64_t)gridDim.x * TAB_WARPS) {
-        const int64_t img = g / N, nn = g - img * N;
+    // work item t -> pixel nn = t / nimg of image t % nimg: every image's
+    // symbols complete front to back at the same rate, which the chasing
+    // range-coder plan (k_rc_plan, chase mode) follows
+    // Work is handed out in TAB_BATCH-item grabs from a global counter, so
+    // production is front to back whatever the block residency.
+    const int64_t nimg = total / N;
+    int64_t tw = 0, tw_end = 0;
+    for (;;) {
+        if (tw >= tw_end) {
+            unsigned long long b0 = 0;
+            if (lane == 0) b0 = atomicAdd(ctr, (unsigned long long)TAB_BATCH);
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if ((int64_t)b0 >= total) break;
+            tw = (int64_t)b0;
+            tw_end = tw + TAB_BATCH < total ? tw + TAB_BATCH : total;
+        }
+        const int64_t t = tw++;
+        const int64_t nn = t / nimg, img = t - nn * nimg;
+        const int64_t g = img * N + nn;
         for (int m = lane; m < M; m += 32) rbuf[wid][m] = __ldg(raw + g * M + m);
         const int32_t ij = __ldg(order + nn);
         const uint8_t* px = images + ((int64_t)img * N + (int64_t)(ij >> 16) * W + (ij & 0xFFFF)) * 3;
@@ -264,16 +282,27 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
 
 template <int VAR>
 void launch_enc_tables_v(bool big, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
-                         const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc, cudaStream_t st) {
-    if (big) k_enc_tables<VAR, true><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc);
-    else k_enc_tables<VAR, false><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc);
+                         const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
+                         unsigned long long* ctr, cudaStream_t st) {
+    if (big) k_enc_tables<VAR, true><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc, ctr);
+    else k_enc_tables<VAR, false><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc, ctr);
+}
+int preload_enc_tables(int var, int K) {
+    const bool big = 3 * K > 32;
+    cudaFuncAttributes fa;
+    cudaError_t e;
+    if (var == 2) e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<2, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<2, false>);
+    else if (var == 1) e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<1, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<1, false>);
+    else e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<0, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<0, false>);
+    return e == cudaSuccess ? 0 : fail(LPIC_E_CUDA, cudaGetErrorString(e));
 }
 void launch_enc_tables(int var, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
-                       const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc, cudaStream_t st) {
+                       const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
+                       unsigned long long* ctr, cudaStream_t st) {
     const bool big = 3 * K > 32;
-    if (var == 2) launch_enc_tables_v<2>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
-    else if (var == 1) launch_enc_tables_v<1>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
-    else launch_enc_tables_v<0>(big, g, raw, M, K, images, W, order, N, total, sw, tc, st);
+    if (var == 2) launch_enc_tables_v<2>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
+    else if (var == 1) launch_enc_tables_v<1>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
+    else launch_enc_tables_v<0>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -365,27 +394,55 @@ constexpr int RC_CH = 1024;
 constexpr int RC_CHUNK = 256;
 static_assert(RC_CH % RC_CHUNK == 0 && (RC_CH & (RC_CH - 1)) == 0, "chunk boundaries on block starts");
 
+constexpr uint32_t RC_PENDING = 0xFFFFFFFFu;    // sw sentinel: start 65535 + width 65536 cannot occur
+__device__ __forceinline__ uint32_t ld_relaxed_sw(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// chase: the symbols are still being produced (k_enc_tables on another
+// stream); wait for each until it is no longer RC_PENDING
 __device__ __forceinline__ void rc_sym_load(const uint32_t* __restrict__ p, int64_t n, int64_t c, int lane,
-                                            uint32_t (&nxt)[RC_CHUNK / 32]) {
+                                            uint32_t (&nxt)[RC_CHUNK / 32], bool chase, bool& timed_out) {
 #pragma unroll
     for (int q = 0; q < RC_CHUNK / 32; q++) {
         const int64_t k = c + 32 * q + lane;
-        nxt[q] = (k < n) ? __ldg(p + k) : 0u;
+        nxt[q] = (k < n) ? (chase ? ld_relaxed_sw(p + k) : __ldg(p + k)) : 0u;
+    }
+    if (chase) {
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) {
+            const int64_t k = c + 32 * q + lane;
+            uint32_t spins = 0;                       // (bounded: a failed producer must not hang the device)
+            while (k < n && nxt[q] == RC_PENDING) {
+                if (++spins > (1u << 26)) { timed_out = true; break; }
+                __nanosleep(256);
+                nxt[q] = ld_relaxed_sw(p + k);
+            }
+        }
     }
 }
 
-__global__ void __launch_bounds__(32)
+// RC_PLAN_WARPS streams per block, one warp each (one per SM sub-partition);
+// in chase mode the block also claims most of the SM's shared memory so no
+// table block shares its SM: the serial chains then issue undisturbed.
+constexpr int RC_PLAN_WARPS = 4;
+__global__ void __launch_bounds__(32 * RC_PLAN_WARPS)
 k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
-          int64_t fixed_cnt, int max_chunks, unsigned long long* __restrict__ Rc, int64_t* __restrict__ posc) {
-    __shared__ uint32_t sbuf[RC_CHUNK];
-    const int s = blockIdx.x, lane = threadIdx.x;
+          int64_t fixed_cnt, int max_chunks, unsigned long long* __restrict__ Rc, int64_t* __restrict__ posc,
+          int chase, int32_t* status, int n_streams) {
+    __shared__ uint32_t sbuf_all[RC_PLAN_WARPS][RC_CHUNK];
+    const int s = blockIdx.x * RC_PLAN_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (s >= n_streams) return;
+    uint32_t* sbuf = sbuf_all[threadIdx.x >> 5];
     const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
     const int64_t n = cnt ? cnt[s] : fixed_cnt;
     const uint32_t* p = sw + base;
     unsigned long long* R_out = Rc + (int64_t)s * max_chunks;
     int64_t* P_out = posc + (int64_t)s * (max_chunks + 1);
     uint32_t nxt[RC_CHUNK / 32];
-    rc_sym_load(p, n, 0, lane, nxt);
+    bool timed_out = false;
+    rc_sym_load(p, n, 0, lane, nxt, chase != 0, timed_out);
     uint64_t R = RC_TOP - 1;
     int64_t S = 0;
     for (int64_t c = 0; c < n; c += RC_CHUNK) {
@@ -393,22 +450,25 @@ k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, cons
 #pragma unroll
         for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
         __syncwarp();
-        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt);
+        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt, chase != 0 && !timed_out, timed_out);
         if (lane == 0) {
             if ((c & (RC_CH - 1)) == 0) { R_out[c / RC_CH] = R; P_out[c / RC_CH] = S; }   // RC_CH % RC_CHUNK == 0
             const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
             uint32_t r = (uint32_t)(R >> 16);
             uint32_t x = sbuf[0];
             uint32_t sb = 0;                                   // shifts in this block
-#pragma unroll 1
+#pragma unroll 4
             for (int k = 0; k < m; k++) {
                 const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
-                // range' = r * width; renormalise by whole bytes (sh <= 2 as r >= 2^24)
-                const uint64_t Pq = (uint64_t)r * ((x & 0xFFFFu) + 1u);
-                const uint32_t hi = (uint32_t)(Pq >> 32);
-                const uint32_t sh = (hi < 0x100u) + (hi == 0u);
-                sb += sh;
-                r = (uint32_t)(Pq >> (16 - 8 * sh));                          // (range' << 8sh) >> 16
+                // range' = r * width; renormalise by whole bytes (sh <= 2 as
+                // r >= 2^24): next r = (range' << 8sh) >> 16.  The three
+                // candidate shifts are formed in parallel and selected, so the
+                // serial chain is multiply -> shift -> two selects.
+                const uint32_t wq = (x & 0xFFFFu) + 1u;
+                const uint32_t hi = __umulhi(r, wq), lo = r * wq;     // 32-bit halves: 32-bit compares
+                const uint32_t r16 = __funnelshift_r(lo, hi, 16), r8 = __funnelshift_r(lo, hi, 8);
+                sb += (hi < 0x100u) + (hi == 0u);
+                r = hi >= 0x100u ? r16 : (hi != 0u ? r8 : lo);
                 x = y;
             }
             S += sb;
@@ -416,6 +476,7 @@ k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, cons
         }
     }
     if (lane == 0) P_out[(n + RC_CH - 1) / RC_CH] = S;
+    if (timed_out && status) atomicOr(status + s, LPIC_S_INTERNAL);
 }
 
 // carry of +1 into byte j, rippling back over 0xFF down to `floor`; returns 1
@@ -517,13 +578,14 @@ k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, co
     RcEncoder e;
     e.init(out + (int64_t)s * cap_each, cap_each);
     uint32_t nxt[RC_CHUNK / 32];
-    rc_sym_load(p, n, 0, lane, nxt);
+    bool no_wait = false;
+    rc_sym_load(p, n, 0, lane, nxt, false, no_wait);
     for (int64_t c = 0; c < n; c += RC_CHUNK) {
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
         __syncwarp();
-        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt);
+        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt, false, no_wait);
         if (lane == 0) {
             const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
             uint32_t x = sbuf[0];
@@ -723,6 +785,11 @@ struct lpic_model {
     uint32_t* d_flags = nullptr; size_t flags_cap = 0;
     uint32_t* d_progress = nullptr; size_t progress_cap = 0;
     unsigned long long* d_dbg = nullptr;   // optional decoder timeline (lpic_decode_debug)
+    // encoder: side stream (high priority) for the chasing range-coder plan
+    cudaStream_t side = nullptr;
+    unsigned long long* d_ctr = nullptr;   // k_enc_tables work counter
+    bool enc_loaded = false;               // encoder kernels preloaded (chase mode)
+    cudaEvent_t ev_sw = nullptr, ev_plan = nullptr;
     int launches = 0;
     std::mutex mu;
 };
@@ -748,12 +815,25 @@ struct RcWork {
 };
 // the three-phase parallel range coder over n streams (fixed count or
 // per-stream off/cnt); max_count bounds every stream's symbol count
-int rc_encode_parallel(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt,
-                       int64_t fixed_cnt, int n, int64_t max_count, uint8_t* d_out, int64_t cap_each,
-                       int64_t* d_lens, int32_t* d_status, cudaStream_t st) {
-    const int max_chunks = (int)((max_count + RC_CH - 1) / RC_CH) > 0 ? (int)((max_count + RC_CH - 1) / RC_CH) : 1;
-    k_rc_plan<<<n, 32, 0, st>>>(d_sw, d_off, d_cnt, fixed_cnt, max_chunks, wk.R, wk.P);
+int rc_max_chunks(int64_t max_count) {
+    return (int)((max_count + RC_CH - 1) / RC_CH) > 0 ? (int)((max_count + RC_CH - 1) / RC_CH) : 1;
+}
+int rc_plan(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt, int64_t fixed_cnt,
+            int n, int64_t max_count, bool chase, int32_t* d_status, cudaStream_t st) {
+    // chase: ~200 KB of (unused) dynamic shared memory reserves the SM
+    const int hog = chase ? 200 * 1024 : 0;
+    if (chase && cudaFuncSetAttribute(k_rc_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, hog) != cudaSuccess)
+        return fail(LPIC_E_CUDA, "k_rc_plan smem attribute");
+    k_rc_plan<<<(n + RC_PLAN_WARPS - 1) / RC_PLAN_WARPS, 32 * RC_PLAN_WARPS, hog, st>>>(
+        d_sw, d_off, d_cnt, fixed_cnt, rc_max_chunks(max_count), wk.R, wk.P, chase ? 1 : 0, d_status, n);
     CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+// phases 2-3 (after the plan)
+int rc_encode_finish(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt,
+                     int64_t fixed_cnt, int n, int64_t max_count, uint8_t* d_out, int64_t cap_each,
+                     int64_t* d_lens, int32_t* d_status, cudaStream_t st) {
+    const int max_chunks = rc_max_chunks(max_count);
     const int64_t threads = (int64_t)n * max_chunks;
     k_rc_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(d_sw, d_off, d_cnt, fixed_cnt, n, max_chunks, wk.R,
                                                                    wk.P, d_out, cap_each, wk.W, wk.C, d_status);
@@ -762,6 +842,12 @@ int rc_encode_parallel(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_
                                                            d_out, cap_each, d_lens, d_status);
     CUDA_TRY(cudaGetLastError());
     return 0;
+}
+int rc_encode_parallel(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt,
+                       int64_t fixed_cnt, int n, int64_t max_count, uint8_t* d_out, int64_t cap_each,
+                       int64_t* d_lens, int32_t* d_status, cudaStream_t st) {
+    if (int r = rc_plan(wk, d_sw, d_off, d_cnt, fixed_cnt, n, max_count, false, d_status, st)) return r;
+    return rc_encode_finish(wk, d_sw, d_off, d_cnt, fixed_cnt, n, max_count, d_out, cap_each, d_lens, d_status, st);
 }
 
 template <typename Kern>
@@ -817,11 +903,46 @@ int launch_enc_net_tc(lpic_model* m, const uint8_t* d_images, int n, int H, int 
     return 0;
 }
 
+// The range-coder plan runs CONCURRENTLY with the table kernel: it is
+// launched on the model's high-priority side stream, follows each image's
+// symbols as they complete (RC_PENDING sentinels) and so finishes right after
+// the last table instead of adding its serial ~1.2 M-symbol chain afterwards.
+struct RcChase {
+    RcWork wk;
+    int64_t count;               // symbols per stream (3N)
+};
+
 template <int CP, int HH> struct EncodeRun {
     static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw, uint32_t* sw,
-                   int32_t* d_status, float* tr, int32_t* tc, cudaStream_t st) {
+                   int32_t* d_status, float* tr, int32_t* tc, const RcChase* chase, cudaStream_t st) {
         constexpr int TC = Taps<HH>::TC;
         const int64_t N = (int64_t)H * W;
+        if (!m->d_ctr && cudaMalloc(&m->d_ctr, sizeof(unsigned long long)) != cudaSuccess)
+            return fail(LPIC_E_NOMEM, "cudaMalloc work counter failed");
+        // chase: the plan goes first (before the network), so its blocks are
+        // resident before the table kernel's persistent blocks fill the GPU.
+        // Every kernel enqueued behind it is loaded first: under lazy module
+        // loading a first launch could otherwise wait behind the spinning plan.
+        if (chase && !m->enc_loaded) {
+            cudaFuncAttributes fa;
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_enc_net<CP, HH>));
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_enc_net_tc<HH>));
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_plan));
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_chunks));
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_merge));
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_pack));
+            for (int var = 0; var < 3; var++)
+                if (int r = preload_enc_tables(var, m->K)) return r;
+            m->enc_loaded = true;
+        }
+        if (chase) {
+            CUDA_TRY(cudaMemsetAsync(sw, 0xFF, sizeof(uint32_t) * (size_t)N * n * 3, st));
+            CUDA_TRY(cudaEventRecord(m->ev_sw, st));
+            CUDA_TRY(cudaStreamWaitEvent(m->side, m->ev_sw, 0));
+            if (int r = rc_plan(chase->wk, sw, nullptr, nullptr, chase->count, n, chase->count, true, d_status, m->side))
+                return r;
+            CUDA_TRY(cudaEventRecord(m->ev_plan, m->side));
+        }
         if (m->precision == LPIC_PREC_FAST) {
             if (int r = launch_enc_net_tc<HH>(m, d_images, n, H, W, mode, raw, d_status, tr, st)) return r;
         } else {
@@ -835,9 +956,10 @@ template <int CP, int HH> struct EncodeRun {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
         const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
-        const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
+        const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 4 ? blocks : (int64_t)sms * 4);   // (dynamic work: >= resident)
+        CUDA_TRY(cudaMemsetAsync(m->d_ctr, 0, sizeof(unsigned long long), st));
         launch_enc_tables((m->precision == LPIC_PREC_FAST && m->dist == 0) ? 2 : m->dist, g2, raw, m->M, m->K, d_images,
-                          W, m->d_order, N, total, sw, tc, st);
+                          W, m->d_order, N, total, sw, tc, m->d_ctr, st);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -1129,6 +1251,10 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_progress);
     cudaFree(m->d_rcR); cudaFree(m->d_rcW); cudaFree(m->d_rcP); cudaFree(m->d_rcC);
     cudaFree(m->d_tc);
+    cudaFree(m->d_ctr);
+    if (m->ev_sw) cudaEventDestroy(m->ev_sw);
+    if (m->ev_plan) cudaEventDestroy(m->ev_plan);
+    if (m->side) cudaStreamDestroy(m->side);
     delete m;
     return 0;
 }
@@ -1273,20 +1399,34 @@ int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, in
     if (int r = ensure(m->d_sw, m->sw_cap, (size_t)n * N * 3)) return r;
     if (int r = ensure(m->d_raw, m->raw_cap, (size_t)n * N * m->M)) return r;
     CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
-    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
-                                    d_trace_raw, d_trace_cdf, st))
-        return r;
-    {
-        const int64_t mc = (3 * N + RC_CH - 1) / RC_CH;
-        if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)n * mc)) return r;
-        if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)n * mc)) return r;
-        if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)n * (mc + 1))) return r;
-        if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)n * mc)) return r;
-        RcWork wk{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC};
-        if (int r = rc_encode_parallel(wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
-                                       d_status, st))
-            return r;
+    if (!m->side) {                                   // created on first use (the library loads without a GPU)
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, hi));
+        CUDA_TRY(cudaEventCreateWithFlags(&m->ev_sw, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&m->ev_plan, cudaEventDisableTiming));
     }
+    const int64_t mc = (3 * N + RC_CH - 1) / RC_CH;
+    if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)n * mc)) return r;
+    if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)n * mc)) return r;
+    if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)n * (mc + 1))) return r;
+    if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)n * mc)) return r;
+    const RcChase chase{RcWork{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC}, 3 * N};
+    // LPIC_NO_CHASE=1: plan after the tables on the caller's stream (for tools
+    // that serialise kernels, e.g. compute-sanitizer)
+    static const bool chase_env = std::getenv("LPIC_NO_CHASE") == nullptr;
+    const bool chase_on = chase_env && n <= 16 * RC_PLAN_WARPS;   // (larger batches: the plan is short next to the tables)
+    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
+                                    d_trace_raw, d_trace_cdf, chase_on ? &chase : nullptr, st))
+        return r;
+    if (chase_on) {
+        CUDA_TRY(cudaStreamWaitEvent(st, m->ev_plan, 0));
+    } else if (int r = rc_plan(chase.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, false, d_status, st)) {
+        return r;
+    }
+    if (int r = rc_encode_finish(chase.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
+                                 d_status, st))
+        return r;
     m->launches = 5;
     return 0;
 }
