@@ -11,17 +11,18 @@
 //      (2K interleaved Phi chains, phi_gauss_vec); lane 31 -> edge slot;
 //      barrier E; PMF with the reference's per-component order and d > 0
 //      rule; exact fixed-point warp partial of the total; barrier T
-//   Q  scale, floor, m = f + 1, remainder fr = v - f, 5-bit remainder digit
-//      d = floor(32 fr); per warp: exclusive prefix of m, and for every
-//      digit value b (lane b) the lanes whose bins have digit b (ten
-//      ballots, no atomics, no zeroing); barrier A
+//   Q  scale, floor, m = f + 1, remainder fr = v - f, 8-bit remainder
+//      digit d = floor(256 fr) into a shared histogram (red.shared.add;
+//      digit 0 -- the tails -- counted per warp with one REDUX; the
+//      histogram is zeroed between E and T); per warp: exclusive prefix of
+//      m; barrier A
 //   S  every warp redundantly (so no further barrier), lane l owning bins
-//      8l..8l+7: deficit; the digit bucket B holding the deficit-th largest
-//      remainder (suffix sums, bit-sliced over lanes); if B is split, its
-//      ~8 members are compacted one per lane and ranked exactly (remainder
-//      desc, index asc == the reference's stable argsort of f - v,
-//      kernels.py:286-290); cdf = prefix of m + prefix of the +1s; symbol
-//      search against the target.
+//      and digits 8l..8l+7: deficit; the digit bucket B holding the
+//      deficit-th largest remainder (suffix sums by a warp scan); if B is
+//      split (it holds ~1-2 bins), its members are ranked exactly
+//      (remainder desc, index asc == the reference's stable argsort of
+//      f - v, kernels.py:286-290); cdf = prefix of m + prefix of the +1s;
+//      symbol search against the target.
 //
 // The arithmetic is bin-for-bin identical to the warp builder (lpic_cdf.cuh
 // warp_table), so encoder and decoder agree (scripts/ubench_chain.cu checks
@@ -42,13 +43,12 @@ struct ChainSmem {
     alignas(16) double frac[256];                 // remainders v - f (selection keys)
     alignas(16) uint32_t mpre[256];               // in-warp exclusive prefix of m (warp = bin >> 6)
     alignas(16) uint32_t mpk[CH_THREADS];         // m of bins 2t | 2t+1 << 16
-    alignas(16) uint8_t dig[256];                 // remainder digits floor(32 fr)
-    alignas(16) uint8_t dig2[256];                // second digits floor(1024 fr) & 31 (0xFF: not in bucket B)
-    alignas(16) uint2 bmask[CH_WARPS][32];        // [warp][digit] = lanes with that digit (bin slot 0, slot 1)
-    alignas(16) uint2 bmask2[CH_WARPS][32];       // the same for the second digit, members of B only
+    alignas(16) uint8_t dig[256];                 // remainder digits floor(256 fr)
     alignas(16) unsigned long long wq[CH_WARPS];  // per-warp fixed-point PMF sums
     alignas(16) int wm[CH_WARPS];                 // per-warp sums of m
     alignas(16) double wedge[CH_WARPS][KMAX];     // each warp's last upper-edge CDF value per component
+    alignas(16) uint32_t hist[256];               // 8-bit remainder-digit histogram (digits 1..255)
+    alignas(16) int wz[CH_WARPS];                 // per-warp count of digit-0 bins
     float wedgeq[CH_WARPS][KMAX];                 // (FAST) last upper edge as (Q, above-zero)
     int wedgep[CH_WARPS][KMAX];
 };
@@ -84,13 +84,6 @@ __device__ __forceinline__ uint32_t bits8(uint32_t lo, uint32_t hi) {
     return ((lo & 0x01010101u) * 0x01020408u >> 24) | (((hi & 0x01010101u) * 0x01020408u >> 24) << 4);
 }
 
-// lanes whose 5-bit digit equals this lane's index
-__device__ __forceinline__ uint32_t digit_lanes(int d, const uint32_t (&inv)[5]) {
-    uint32_t m = 0xffffffffu;
-#pragma unroll
-    for (int j = 0; j < 5; j++) m &= __ballot_sync(0xffffffffu, (d >> j) & 1) ^ inv[j];
-    return m;
-}
 
 // KU > 0: compile-time component count; KU == 0: runtime K (<= KMAX)
 // want_sym < 0: decoder -- find the symbol whose interval holds `target`;
@@ -137,6 +130,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);
+    reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
     float f0 = 0.0f, f1 = 0.0f;
 #pragma unroll
     for (int q = 0; q < KC; q++) {
@@ -176,6 +170,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             z[2 * q] = __dmul_rn(__dsub_rn(e0, mu), iv);
             z[2 * q + 1] = __dmul_rn(__dsub_rn(e1, mu), iv);
         }
+        CHP(11);
         if (KU > 0 && dist == 0) {
 #ifdef ABL_NOPHI
 #pragma unroll
@@ -190,6 +185,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                 cur[i] = cdf_value(z[i], dist, cc->phic);
             }
         }
+        CHP(12);
         if (k0 + 1 == 255) {
 #pragma unroll
             for (int q = 0; q < KC; q++) cur[2 * q + 1] = 1.0;          // kernels.py:263
@@ -205,6 +201,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);
+    reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
     // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
     p0 = 0.0; p1 = 0.0;
 #pragma unroll
@@ -251,16 +248,18 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             m0 = (int)f0 + 1; m1 = (int)f1 + 1;
             fr0 = __dsub_rn(v0, f0); fr1 = __dsub_rn(v1, f1);     // == -(f - v) exactly
         }
-        const int d0 = min(__double2int_rz(__dmul_rn(fr0, 32.0)), 31);
-        const int d1 = min(__double2int_rz(__dmul_rn(fr1, 32.0)), 31);
+        // 8-bit remainder digit; histogram in shared memory (digit 0 -- the
+        // tails, where most bins would collide -- counted per warp instead)
+        const int d0 = min(__double2int_rz(__dmul_rn(fr0, 256.0)), 255);
+        const int d1 = min(__double2int_rz(__dmul_rn(fr1, 256.0)), 255);
+        if (d0) atomicAdd(cs->hist + d0, 1u);
+        if (d1) atomicAdd(cs->hist + d1, 1u);
+        const int zc = __reduce_add_sync(0xffffffffu, (d0 == 0) + (d1 == 0));
+        if (lane == 0) cs->wz[w] = zc;
         reinterpret_cast<double2*>(cs->frac)[t] = make_double2(fr0, fr1);
         reinterpret_cast<uint16_t*>(cs->dig)[t] = (uint16_t)(d0 | (d1 << 8));
         cs->mpk[t] = (uint32_t)m0 | ((uint32_t)m1 << 16);
         const int ms = __reduce_add_sync(0xffffffffu, m0 + m1);
-        uint32_t inv[5];
-#pragma unroll
-        for (int j = 0; j < 5; j++) inv[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
-        cs->bmask[w][lane] = make_uint2(digit_lanes(d0, inv), digit_lanes(d1, inv));
         // in-warp exclusive prefix of m in bin order (bins 2t, 2t+1)
         const uint32_t pr = (uint32_t)(m0 + m1);
         uint32_t incl = pr;
@@ -289,61 +288,43 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
 #else
     if (deficit > 0) {
 #endif
-        // level 1 -- digit counts: lane b <-> digit b
-        int B, nB, need;
+        // 8-bit digit bucket B holding the deficit-th largest remainder: lane
+        // l reads the counts of digits 8l..8l+7, suffix sums by a warp scan
         {
-            const uint2 k0m = cs->bmask[0][lane], k1m = cs->bmask[1][lane], k2m = cs->bmask[2][lane],
-                        k3m = cs->bmask[3][lane];
-            const int cnt = (__popc(k0m.x) + __popc(k0m.y) + __popc(k1m.x) + __popc(k1m.y)) +
-                            (__popc(k2m.x) + __popc(k2m.y) + __popc(k3m.x) + __popc(k3m.y));
-            const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);      // bins with digit >= lane
-            B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));          // deficit <= 256 = S(0)
-            nB = __shfl_sync(0xffffffffu, cnt, B);
-            need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);            // 1 <= need <= nB
-        }
-        CHP(13);
-        const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
-        bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
-        const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
-        if (need == nB) {
-            bm |= mem;
-        } else {
-            // level 2 among the members of B (uniform branch): second digit,
-            // per-warp ballots over this warp's own bins, one more barrier
-            {
-                const double2 fr2 = reinterpret_cast<const double2*>(cs->frac)[t];
-                const uint16_t dd = reinterpret_cast<const uint16_t*>(cs->dig)[t];
-                const bool in0 = (dd & 0xFF) == B, in1 = (dd >> 8) == B;
-                const int e0d = (int)(__double2ull_rz(__dmul_rn(fr2.x, 1024.0)) & 31u);
-                const int e1d = (int)(__double2ull_rz(__dmul_rn(fr2.y, 1024.0)) & 31u);
-                uint32_t inv[5];
+            const uint4 ha = reinterpret_cast<const uint4*>(cs->hist)[2 * lane];
+            const uint4 hb = reinterpret_cast<const uint4*>(cs->hist)[2 * lane + 1];
+            int c[8] = {(int)ha.x, (int)ha.y, (int)ha.z, (int)ha.w, (int)hb.x, (int)hb.y, (int)hb.z, (int)hb.w};
+            if (lane == 0) {
+                const int4 z4 = *reinterpret_cast<const int4*>(cs->wz);
+                c[0] = (z4.x + z4.y) + (z4.z + z4.w);
+            }
+            int sfx[8];
+            sfx[7] = c[7];
 #pragma unroll
-                for (int j = 0; j < 5; j++) inv[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
-                cs->bmask2[w][lane] = make_uint2(digit_lanes(e0d, inv) & __ballot_sync(0xffffffffu, in0),
-                                                 digit_lanes(e1d, inv) & __ballot_sync(0xffffffffu, in1));
-                reinterpret_cast<uint16_t*>(cs->dig2)[t] = (uint16_t)((in0 ? e0d : 0xFF) | ((in1 ? e1d : 0xFF) << 8));
+            for (int q = 6; q >= 0; q--) sfx[q] = sfx[q + 1] + c[q];
+            int incl = sfx[0];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += u;
             }
-            chain_sync(bar);                                                                // A2
-            int B2, n2, need2;
-            {
-                const uint2 k0m = cs->bmask2[0][lane], k1m = cs->bmask2[1][lane], k2m = cs->bmask2[2][lane],
-                            k3m = cs->bmask2[3][lane];
-                const int cnt = (__popc(k0m.x) + __popc(k0m.y) + __popc(k1m.x) + __popc(k1m.y)) +
-                                (__popc(k2m.x) + __popc(k2m.y) + __popc(k3m.x) + __popc(k3m.y));
-                const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
-                B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
-                n2 = __shfl_sync(0xffffffffu, cnt, B2);
-                need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
-            }
-            const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
-            const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
-            // non-members carry 0xFF: mask them with mem
-            bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
-            const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
-            if (need2 == n2) {
-                bm |= mem2;
+            const int above = incl - sfx[0];
+            int qb = -1, nb_l = 0, sb_l = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (sfx[q] + above >= deficit) { qb = q; nb_l = c[q]; sb_l = sfx[q] + above; }
+            const int L = 31 - __clz(__ballot_sync(0xffffffffu, qb >= 0));
+            const int B = 8 * L + __shfl_sync(0xffffffffu, qb, L);
+            const int nB = __shfl_sync(0xffffffffu, nb_l, L);
+            const int need = deficit - (__shfl_sync(0xffffffffu, sb_l, L) - nB);   // 1 <= need <= nB
+            CHP(13);
+            const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
+            bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
+            const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
+            if (need == nB) {
+                bm |= mem;
             } else {
-                // rare: exact ranks among the members of (B, B2), frac desc / index asc
+                // exact ranks among the (few) members of B, frac desc / index asc
                 double fr[8];
                 const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
 #pragma unroll
@@ -351,11 +332,11 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                 int rank[8];
 #pragma unroll
                 for (int q = 0; q < 8; q++) rank[q] = 0;
-                uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
+                uint32_t lanes = __ballot_sync(0xffffffffu, mem != 0);
                 while (lanes) {
                     const int src = __ffs(lanes) - 1;
                     lanes &= lanes - 1;
-                    uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
+                    uint32_t qs = __shfl_sync(0xffffffffu, mem, src);
                     while (qs) {
                         const int q2 = __ffs(qs) - 1;
                         qs &= qs - 1;
@@ -366,7 +347,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
+                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem >> q) & 1) && rank[q] < need) << q;
             }
         }
     }
@@ -407,267 +388,6 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
         if (lane == 31) trace_row[256] = 65536;
     }
-    CHP(9);
-}
-
-// ---------------------------------------------------------------------------
-// chain_table1: the same table with 256 chain threads, ONE bin per thread
-// (8 warps, two per SM sub-partition, so warp-level parallelism hides the
-// latency that a single warp per sub-partition exposes).  Same arithmetic
-// and selection as chain_table; post-barrier work is redundant per warp.
-// ---------------------------------------------------------------------------
-constexpr int C1_THREADS = 256;
-constexpr int C1_WARPS = 8;
-__device__ __forceinline__ void chain_sync1() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-struct ChainSmem1 {
-    alignas(16) double frac[256];
-    alignas(16) uint32_t mpre[256];               // in-warp exclusive prefix of m (warp = bin >> 5)
-    alignas(16) uint16_t mv[256];                 // m per bin
-    alignas(16) uint8_t dig[256];
-    alignas(16) uint8_t dig2[256];
-    alignas(16) uint32_t bmask[C1_WARPS][32];
-    alignas(16) uint32_t bmask2[C1_WARPS][32];
-    alignas(16) unsigned long long wq[C1_WARPS];
-    alignas(16) int wm[C1_WARPS];
-    alignas(16) double wedge[C1_WARPS][KMAX];
-    uint32_t res[4];                              // (sym, start, mass) for warps 4-7
-};
-
-template <int KU, bool BLUE>
-__device__ __forceinline__ void chain_table1(const double* __restrict__ pi, const double* __restrict__ inv,
-                                             const float* __restrict__ mu0, const float* __restrict__ t1,
-                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
-                                             const CdfConsts* __restrict__ cc, ChainSmem1* __restrict__ cs,
-                                             uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
-                                             int32_t* trace_row, int want_sym = -1) {
-    constexpr int KC = KU > 0 ? KU : KMAX;
-    const int K = KU > 0 ? KU : Kr;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;   // bin t
-    CHP0;
-    // ---- P
-    const double e0 = cc->edges[t + 1];
-    double cur[KC];
-    {
-        double z[KC];
-#pragma unroll
-        for (int q = 0; q < KC; q++) {
-            if (KU == 0 && q >= K) { z[q] = 0.0; continue; }
-            const float m32 = BLUE ? __fadd_rn(__fadd_rn(mu0[q], __fmul_rn(t1[q], rn)), __fmul_rn(t2[q], gn))
-                                   : __fadd_rn(mu0[q], __fmul_rn(t1[q], rn));      // kernels.py:236-240
-            z[q] = __dmul_rn(__dsub_rn(e0, (double)m32), inv[q]);
-        }
-        if (KU > 0 && dist == 0) {
-            double t_[KC];
-            const double2* row[KC];
-#pragma unroll
-            for (int i = 0; i < KC; i++) row[i] = phi_row(z[i], t_[i], cc->phic);
-#pragma unroll
-            for (int i = 0; i < KC; i++) { const double2 c = row[i][LPIC_PHI_ROW / 2 - 1]; cur[i] = __fma_rn(c.y, t_[i], c.x); }
-#pragma unroll
-            for (int j = LPIC_PHI_ROW / 2 - 2; j >= 0; j--) {
-#pragma unroll
-                for (int i = 0; i < KC; i++) { const double2 c = row[i][j]; cur[i] = __fma_rn(__fma_rn(cur[i], t_[i], c.y), t_[i], c.x); }
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < KC; i++) {
-                if (KU == 0 && i >= K) break;
-                cur[i] = cdf_value(z[i], dist, cc->phic);
-            }
-        }
-        if (t == 255) {
-#pragma unroll
-            for (int q = 0; q < KC; q++) cur[q] = 1.0;                   // kernels.py:263
-        }
-    }
-    if (lane == 31) {
-#pragma unroll
-        for (int q = 0; q < KC; q++) {
-            if (KU == 0 && q >= K) break;
-            cs->wedge[w][q] = cur[q];
-        }
-    }
-    CHP(0);
-    chain_sync1();                                                                       // E
-    CHP(1);
-    double p0 = 0.0;
-#pragma unroll
-    for (int q = 0; q < KC; q++) {
-        if (KU == 0 && q >= K) break;
-        double prev = __shfl_up_sync(0xffffffffu, cur[q], 1);
-        if (lane == 0) prev = (w == 0) ? 0.0 : cs->wedge[w - 1][q];
-        const double d0 = __dsub_rn(cur[q], prev);
-        const double n0 = __dadd_rn(p0, __dmul_rn(pi[q], d0));
-        p0 = d0 > 0.0 ? n0 : p0;
-    }
-    {
-        const unsigned long long wsum = fx_warp_sum(fx_bin(p0));
-        if (lane == 0) cs->wq[w] = wsum;
-    }
-    CHP(2);
-    chain_sync1();                                                                       // T
-    CHP(3);
-    {
-        const ulonglong2 q01 = reinterpret_cast<const ulonglong2*>(cs->wq)[0];
-        const ulonglong2 q23 = reinterpret_cast<const ulonglong2*>(cs->wq)[1];
-        const ulonglong2 q45 = reinterpret_cast<const ulonglong2*>(cs->wq)[2];
-        const ulonglong2 q67 = reinterpret_cast<const ulonglong2*>(cs->wq)[3];
-        const double scale = cdf_scale(fx_total(((q01.x + q01.y) + (q23.x + q23.y)) + ((q45.x + q45.y) + (q67.x + q67.y))));
-        CHP(10);
-        const double v0 = __dmul_rn(p0, scale);
-        double f0 = floor(v0);
-        f0 = f0 > CDF_FLOOR ? CDF_FLOOR : f0;
-        const int m0 = (int)f0 + 1;
-        const double fr0 = __dsub_rn(v0, f0);
-        const int d0 = min(__double2int_rz(__dmul_rn(fr0, 32.0)), 31);
-        cs->frac[t] = fr0;
-        cs->dig[t] = (uint8_t)d0;
-        cs->mv[t] = (uint16_t)m0;
-        const int ms = __reduce_add_sync(0xffffffffu, m0);
-        uint32_t invm[5];
-#pragma unroll
-        for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
-        cs->bmask[w][lane] = digit_lanes(d0, invm);
-        uint32_t incl = (uint32_t)m0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        cs->mpre[t] = incl - (uint32_t)m0;
-        if (lane == 0) cs->wm[w] = ms;
-    }
-    CHP(4);
-    chain_sync1();                                                                       // A
-    CHP(5);
-    // ---- S, part 1 (all 8 warps): deficit, the level-1 threshold digit, and
-    // -- if that bucket is split -- the level-2 digit masks of each warp's bins
-    int wmv[C1_WARPS];
-    {
-        const int4 a = reinterpret_cast<const int4*>(cs->wm)[0], b = reinterpret_cast<const int4*>(cs->wm)[1];
-        wmv[0] = a.x; wmv[1] = a.y; wmv[2] = a.z; wmv[3] = a.w; wmv[4] = b.x; wmv[5] = b.y; wmv[6] = b.z; wmv[7] = b.w;
-    }
-    const int deficit = 65536 - (((wmv[0] + wmv[1]) + (wmv[2] + wmv[3])) + ((wmv[4] + wmv[5]) + (wmv[6] + wmv[7])));
-    int B = 0, nB = 0, need = 0;
-    if (deficit > 0) {
-        int cnt = 0;
-#pragma unroll
-        for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask[v][lane]);
-        const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
-        B = 31 - __clz(__ballot_sync(0xffffffffu, S >= deficit));
-        nB = __shfl_sync(0xffffffffu, cnt, B);
-        need = deficit - (__shfl_sync(0xffffffffu, S, B) - nB);
-        if (need < nB) {                                   // uniform across the CTA
-            const bool in0 = cs->dig[t] == B;
-            const int e0d = (int)(__double2ull_rz(__dmul_rn(cs->frac[t], 1024.0)) & 31u);
-            uint32_t invm[5];
-#pragma unroll
-            for (int j = 0; j < 5; j++) invm[j] = ((lane >> j) & 1) ? 0u : 0xffffffffu;
-            cs->bmask2[w][lane] = digit_lanes(e0d, invm) & __ballot_sync(0xffffffffu, in0);
-            cs->dig2[t] = (uint8_t)(in0 ? e0d : 0xFF);
-            chain_sync1();                                                               // A2
-        }
-    }
-    CHP(13);
-    // ---- S, part 2 (warps 0-3, redundantly): lane l owns bins 8l..8l+7 (warp l >> 2)
-    if (w < 4) {
-        const int lw = lane >> 2;
-        uint32_t mbase = 0;
-#pragma unroll
-        for (int v = 0; v < C1_WARPS - 1; v++) mbase += (v < lw) ? (uint32_t)wmv[v] : 0u;
-        const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
-        uint32_t bm = 0;
-        if (deficit > 0) {
-            const uint32_t Bx4 = (uint32_t)B * 0x01010101u;
-            bm = bits8(__vcmpgtu4(dg.x, Bx4), __vcmpgtu4(dg.y, Bx4));
-            const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
-            if (need == nB) {
-                bm |= mem;
-            } else {
-                int B2, n2, need2;
-                {
-                    int cnt = 0;
-#pragma unroll
-                    for (int v = 0; v < C1_WARPS; v++) cnt += __popc(cs->bmask2[v][lane]);
-                    const int S = lanes_sum_masked<9>(cnt, 0xffffffffu << lane);
-                    B2 = 31 - __clz(__ballot_sync(0xffffffffu, S >= need));
-                    n2 = __shfl_sync(0xffffffffu, cnt, B2);
-                    need2 = need - (__shfl_sync(0xffffffffu, S, B2) - n2);
-                }
-                const uint2 dg2 = reinterpret_cast<const uint2*>(cs->dig2)[lane];
-                const uint32_t B2x4 = (uint32_t)B2 * 0x01010101u;
-                bm |= mem & bits8(__vcmpgtu4(dg2.x, B2x4), __vcmpgtu4(dg2.y, B2x4));
-                const uint32_t mem2 = mem & bits8(__vcmpeq4(dg2.x, B2x4), __vcmpeq4(dg2.y, B2x4));
-                if (need2 == n2) {
-                    bm |= mem2;
-                } else {
-                    double fr[8];
-                    const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
-#pragma unroll
-                    for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
-                    int rank[8];
-#pragma unroll
-                    for (int q = 0; q < 8; q++) rank[q] = 0;
-                    uint32_t lanes = __ballot_sync(0xffffffffu, mem2 != 0);
-                    while (lanes) {
-                        const int src = __ffs(lanes) - 1;
-                        lanes &= lanes - 1;
-                        uint32_t qs = __shfl_sync(0xffffffffu, mem2, src);
-                        while (qs) {
-                            const int q2 = __ffs(qs) - 1;
-                            qs &= qs - 1;
-                            const int j = 8 * src + q2;
-                            const double f = cs->frac[j];
-#pragma unroll
-                            for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem2 >> q) & 1) && rank[q] < need2) << q;
-                }
-            }
-        }
-        CHP(6);
-        const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
-        const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
-        const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
-        const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
-        uint32_t cdf[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
-        CHP(7);
-        int L, qs = 0;
-        if (want_sym >= 0) {
-            L = want_sym >> 3;
-            qs = want_sym & 7;
-        } else {
-            L = 31 - __clz(__ballot_sync(0xffffffffu, cdf[0] <= target));
-#pragma unroll
-            for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
-        }
-        const uint4 mk = reinterpret_cast<const uint4*>(cs->mv)[lane];
-        const uint32_t mw4[4] = {mk.x, mk.y, mk.z, mk.w};
-        uint32_t st_mine = cdf[0], ms_mine = 0;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            if (q == qs) {
-                st_mine = cdf[q];
-                ms_mine = ((mw4[q >> 1] >> (16 * (q & 1))) & 0xFFFFu) + ((bm >> q) & 1u);
-            }
-        }
-        sym = 8 * L + __shfl_sync(0xffffffffu, qs, L);
-        start = __shfl_sync(0xffffffffu, st_mine, L);
-        mass = __shfl_sync(0xffffffffu, ms_mine, L);
-        if (w == 0 && lane == 0) { cs->res[0] = (uint32_t)sym; cs->res[1] = start; cs->res[2] = mass; }
-        if (trace_row && w == 0) {
-#pragma unroll
-            for (int q = 0; q < 8; q++) trace_row[8 * lane + q] = (int32_t)cdf[q];
-            if (lane == 31) trace_row[256] = 65536;
-        }
-    }
-    chain_sync1();                                                                       // R
-    if (w >= 4) { sym = (int)cs->res[0]; start = cs->res[1]; mass = cs->res[2]; }
     CHP(9);
 }
 

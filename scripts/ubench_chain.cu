@@ -15,15 +15,9 @@ __shared__ long long s_prof[16];     // shared accumulator: no global latency in
 #endif
 #include "lpic_chain.cuh"
 using namespace lpic;
-#ifdef CH1
-#define CT chain_table1
-#define CSM ChainSmem1
-#define NTH 256
-#else
 #define CT chain_table
 #define CSM ChainSmem
 #define NTH 128
-#endif
 
 struct Case { float raw[36]; float rn, gn; uint32_t target; int ch; };
 
@@ -106,7 +100,7 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(NTH) k_time(int tables, long long* out) {
+__global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ __align__(16) CSM cs;
     __shared__ double pi[4], inv[4];
@@ -173,7 +167,7 @@ int main() {
 #ifdef PROF
     long long hp[16]; cudaMemcpyFromSymbol(hp, g_prof, sizeof(hp));
     const char* nm[14] = {"P cdf", "bar E", "pmf+fx", "bar T", "Q rest", "bar A", "S level2+", "prefix", "-", "D search",
-                          "Q scale", "-", "-", "S level1"};
+                          "Q scale", "P z", "P phi", "S level1"};
     for (int i = 0; i < 14; i++) printf("  %-10s %6lld cycles/table\n", nm[i], hp[i] / 4000);
 #endif
     printf("TOTAL mismatches %d\n", total_bad);
