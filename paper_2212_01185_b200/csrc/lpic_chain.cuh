@@ -41,7 +41,6 @@ __device__ __forceinline__ void chain_sync(int id = 1) { asm volatile("bar.sync 
 
 struct ChainSmem {
     alignas(16) double frac[256];                 // remainders v - f (selection keys)
-    alignas(16) uint32_t mpre[256];               // in-warp exclusive prefix of m (warp = bin >> 6)
     alignas(16) uint32_t mpk[CH_THREADS];         // m of bins 2t | 2t+1 << 16
     alignas(16) uint8_t dig[256];                 // remainder digits floor(256 fr)
     alignas(16) unsigned long long wq[CH_WARPS];  // per-warp fixed-point PMF sums
@@ -260,15 +259,6 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         reinterpret_cast<uint16_t*>(cs->dig)[t] = (uint16_t)(d0 | (d1 << 8));
         cs->mpk[t] = (uint32_t)m0 | ((uint32_t)m1 << 16);
         const int ms = __reduce_add_sync(0xffffffffu, m0 + m1);
-        // in-warp exclusive prefix of m in bin order (bins 2t, 2t+1)
-        const uint32_t pr = (uint32_t)(m0 + m1);
-        uint32_t incl = pr;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        reinterpret_cast<uint2*>(cs->mpre)[t] = make_uint2(incl - pr, incl - pr + (uint32_t)m0);
         if (lane == 0) cs->wm[w] = ms;
     }
     CHP(4);
@@ -278,41 +268,54 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     // ---- S: lane l owns bins 8l..8l+7 (all in warp l >> 3)
     const int4 wm4 = *reinterpret_cast<const int4*>(cs->wm);
     const int deficit = 65536 - ((wm4.x + wm4.y) + (wm4.z + wm4.w));
-    const int lw = lane >> 3;
-    const uint32_t mbase = lw == 0 ? 0u : (lw == 1 ? (uint32_t)wm4.x : (lw == 2 ? (uint32_t)(wm4.x + wm4.y)
-                                                                                : (uint32_t)(wm4.x + wm4.y + wm4.z)));
     const uint2 dg = reinterpret_cast<const uint2*>(cs->dig)[lane];
+    // m of this lane's bins, and the digit counts of digits 8l..8l+7
+    const uint4 mk = reinterpret_cast<const uint4*>(cs->mpk)[lane];
+    const uint32_t mv[4] = {mk.x, mk.y, mk.z, mk.w};
+    int c[8];
+    {
+        const uint4 ha = reinterpret_cast<const uint4*>(cs->hist)[2 * lane];
+        const uint4 hb = reinterpret_cast<const uint4*>(cs->hist)[2 * lane + 1];
+        c[0] = (int)ha.x; c[1] = (int)ha.y; c[2] = (int)ha.z; c[3] = (int)ha.w;
+        c[4] = (int)hb.x; c[5] = (int)hb.y; c[6] = (int)hb.z; c[7] = (int)hb.w;
+        if (lane == 0) {
+            const int4 z4 = *reinterpret_cast<const int4*>(cs->wz);
+            c[0] = (z4.x + z4.y) + (z4.z + z4.w);
+        }
+    }
+    // ONE warp scan for both prefixes over lanes: m (<= 65536, 17 bits) and
+    // the digit counts (<= 256, 9 bits) packed as m << 9 | count
+    uint32_t mpl[8], cpl[8];                                // in-lane exclusive prefixes
+    mpl[0] = 0; cpl[0] = 0;
+#pragma unroll
+    for (int q = 1; q < 8; q++) {
+        mpl[q] = mpl[q - 1] + ((mv[(q - 1) >> 1] >> (16 * ((q - 1) & 1))) & 0xFFFFu);
+        cpl[q] = cpl[q - 1] + (uint32_t)c[q - 1];
+    }
+    const uint32_t packed = ((mpl[7] + (mv[3] >> 16)) << 9) | (cpl[7] + (uint32_t)c[7]);
+    uint32_t incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const uint32_t excl = incl - packed;
+    const uint32_t mbase = excl >> 9, hbase = excl & 511u;   // m and digit counts of lower lanes
     uint32_t bm = 0;                                        // bit q: bin 8l+q gets the +1
 #ifdef ABL_NOSEL
     if (deficit > 100000) {
 #else
     if (deficit > 0) {
 #endif
-        // 8-bit digit bucket B holding the deficit-th largest remainder: lane
-        // l reads the counts of digits 8l..8l+7, suffix sums by a warp scan
+        // 8-bit digit bucket B holding the deficit-th largest remainder:
+        // #digits >= b is 256 - (#digits < b), so B is the last digit whose
+        // lower count is <= 256 - deficit
         {
-            const uint4 ha = reinterpret_cast<const uint4*>(cs->hist)[2 * lane];
-            const uint4 hb = reinterpret_cast<const uint4*>(cs->hist)[2 * lane + 1];
-            int c[8] = {(int)ha.x, (int)ha.y, (int)ha.z, (int)ha.w, (int)hb.x, (int)hb.y, (int)hb.z, (int)hb.w};
-            if (lane == 0) {
-                const int4 z4 = *reinterpret_cast<const int4*>(cs->wz);
-                c[0] = (z4.x + z4.y) + (z4.z + z4.w);
-            }
-            int sfx[8];
-            sfx[7] = c[7];
-#pragma unroll
-            for (int q = 6; q >= 0; q--) sfx[q] = sfx[q + 1] + c[q];
-            int incl = sfx[0];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_down_sync(0xffffffffu, incl, o);
-                if (lane + o < 32) incl += u;
-            }
-            const int above = incl - sfx[0];
+            const uint32_t lim = 256u - (uint32_t)deficit;
             int qb = -1, nb_l = 0, sb_l = 0;
 #pragma unroll
             for (int q = 0; q < 8; q++)
-                if (sfx[q] + above >= deficit) { qb = q; nb_l = c[q]; sb_l = sfx[q] + above; }
+                if (hbase + cpl[q] <= lim) { qb = q; nb_l = c[q]; sb_l = 256 - (int)(hbase + cpl[q]); }
             const int L = 31 - __clz(__ballot_sync(0xffffffffu, qb >= 0));
             const int B = 8 * L + __shfl_sync(0xffffffffu, qb, L);
             const int nB = __shfl_sync(0xffffffffu, nb_l, L);
@@ -354,12 +357,9 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     CHP(6);
     // ---- cdf (kernels.py:291-293) = prefix of m + prefix of the +1s; search (coder.py:104)
     const uint32_t bpre = (uint32_t)lanes_sum_masked<4>(__popc(bm), (1u << lane) - 1u);
-    const uint4 mpa = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane];
-    const uint4 mpb = reinterpret_cast<const uint4*>(cs->mpre)[2 * lane + 1];
-    const uint32_t mp[8] = {mpa.x, mpa.y, mpa.z, mpa.w, mpb.x, mpb.y, mpb.z, mpb.w};
     uint32_t cdf[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++) cdf[q] = mbase + mp[q] + bpre + __popc(bm & ((1u << q) - 1u));
+    for (int q = 0; q < 8; q++) cdf[q] = mbase + mpl[q] + bpre + __popc(bm & ((1u << q) - 1u));
     CHP(7);
     int L, qs = 0;
     if (want_sym >= 0) {
@@ -370,8 +370,6 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
 #pragma unroll
         for (int q = 1; q < 8; q++) qs += (cdf[q] <= target);
     }
-    const uint4 mk = reinterpret_cast<const uint4*>(cs->mpk)[lane];
-    const uint32_t mv[4] = {mk.x, mk.y, mk.z, mk.w};
     uint32_t st_mine = cdf[0], ms_mine = 0;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
