@@ -89,17 +89,25 @@ __device__ __forceinline__ uint32_t bits8(uint32_t lo, uint32_t hi) {
 // want_sym >= 0: encoder -- return that symbol's (start, mass).
 // F32: FAST-precision tables (float32 Phi/PMF/quantisation, lpic_cdf.cuh),
 // bin-for-bin identical to warp_pmf32 / warp_quantize32.
-template <int KU, bool BLUE, bool F32 = false>
+// tgt: the range-decoder target, or a callable producing it -- called in the
+// shadow of the Phi phase, so the decoder's advance/target arithmetic for
+// this symbol is off the critical path.
+__device__ __forceinline__ uint32_t chain_target(uint32_t v) { return v; }
+template <class F>
+__device__ __forceinline__ uint32_t chain_target(F& f) { return f(); }
+
+template <int KU, bool BLUE, bool F32 = false, class Tgt = uint32_t>
 __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const double* __restrict__ inv,
                                             const float* __restrict__ mu0, const float* __restrict__ t1,
                                             const float* __restrict__ t2, float rn, float gn, int Kr, int dist,
                                             const CdfConsts* __restrict__ cc, ChainSmem* __restrict__ cs,
-                                            uint32_t target, int& sym, uint32_t& start, uint32_t& mass,
+                                            Tgt&& tgt, int& sym, uint32_t& start, uint32_t& mass,
                                             int32_t* trace_row, int want_sym = -1, int bar = 1) {
     constexpr int KC = KU > 0 ? KU : KMAX;
     const int K = KU > 0 ? KU : Kr;
     const int t = threadIdx.x & (CH_THREADS - 1), lane = t & 31, w = t >> 5;   // chain-local thread
     const int k0 = 2 * t;                                   // bins k0, k0 + 1
+    uint32_t target = 0;
     CHP0;
 
     double p0 = 0.0, p1 = 0.0;
@@ -126,6 +134,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             cs->wedgeq[w][q] = qb[q]; cs->wedgep[w][q] = pb[q];
         }
     }
+    target = chain_target(tgt);
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);
@@ -197,6 +206,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             cs->wedge[w][q] = cur[2 * q + 1];
         }
     }
+    target = chain_target(tgt);
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);

@@ -420,6 +420,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned
         uint64_t r;
         uint32_t target = dec.target(r);
         int sr;
+        uint32_t red_start, red_width;
         {
             const uint4 v = reinterpret_cast<const uint4*>(rv.red)[lane];
             const uint32_t e[4] = {v.x, v.y, v.z, v.w};
@@ -429,7 +430,7 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned
             sr = __reduce_add_sync(0xffffffffu, c) - 1;
             const uint32_t rs = rv.red[sr];
             const uint32_t re = sr == 255 ? 65536u : (uint32_t)rv.red[sr + 1];
-            dec.advance(r, rs, re - rs);
+            red_start = rs; red_width = re - rs;          // (advanced inside the green table's Phi phase)
             if (trow) {
                 trow[2 * ct] = rv.red[2 * ct];
                 trow[2 * ct + 1] = rv.red[2 * ct + 1];
@@ -439,20 +440,22 @@ __device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned
         const float rn = cc->lut[sr];
         if (dbg && ct == 0) dbg[4] = clock64();
         // ---- green: mu_g += tanh(alpha)*rn (kernels.py:236-237)
+        // (the decoder's advance past the previous symbol and the next target
+        // are computed inside each table's Phi phase, off the critical path)
         int sg;
         uint32_t st, ms;
-        target = dec.target(r);
-        chain_table<KU, false, F32>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, target, sg,
+        auto tgt_g = [&]() { dec.advance_bf(r, red_start, red_width); return dec.target(r); };
+        chain_table<KU, false, F32>(rv.pi_g, rv.inv_g, rv.mu_g, rv.ta, nullptr, rn, 0.0f, K, P.dist, cc, ch, tgt_g, sg,
                                st, ms, trow ? trow + 257 : nullptr, -1, bar);
-        dec.advance(r, st, ms);
         const float gn = cc->lut[sg];
         if (dbg && ct == 0) dbg[6] = clock64();
         // ---- blue: mu_b += tanh(beta)*rn + tanh(gamma)*gn (kernels.py:238-240)
         int sb;
-        target = dec.target(r);
-        chain_table<KU, true, F32>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, target, sb, st,
+        const uint32_t g_start = st, g_width = ms;
+        auto tgt_b = [&]() { dec.advance_bf(r, g_start, g_width); return dec.target(r); };
+        chain_table<KU, true, F32>(rv.pi_b, rv.inv_b, rv.mu_b, rv.tb, rv.tc, rn, gn, K, P.dist, cc, ch, tgt_b, sb, st,
                               ms, trow ? trow + 514 : nullptr, -1, bar);
-        dec.advance(r, st, ms);
+        dec.advance_bf(r, st, ms);
         if (dbg && ct == 0) dbg[8] = clock64();
         if (ct == 0) {                                // (slot s was last read before the blue table's barrier A)
             mbar_arrive(&cs->empty[s]);

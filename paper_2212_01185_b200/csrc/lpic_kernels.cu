@@ -305,70 +305,6 @@ void launch_enc_tables(int var, unsigned g, const float* raw, int M, int K, cons
     else launch_enc_tables_v<0>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
 }
 
-// ---------------------------------------------------------------------------
-// encoder, stage 2 (throughput form): one 128-thread CTA per pixel at a time,
-// the three tables built by the chain builder (lpic_chain.cuh) in symbol-
-// lookup mode -- identical tables to the decoder's, no shared-memory
-// atomics, ~10 CTAs per SM (codec.py:168-182, kernels.py:212-313)
-// ---------------------------------------------------------------------------
-struct EncTabSmem {
-    alignas(16) CdfConsts cc;
-    alignas(16) ChainSmem ch;
-    alignas(16) float raw[12 * KMAX];
-    alignas(16) double pi[3][KMAX];
-    alignas(16) double inv[3][KMAX];
-    alignas(16) float mu0[3][KMAX];
-    alignas(16) float ta[KMAX], tb[KMAX], tc[KMAX], zero[KMAX];
-};
-
-template <int KU>
-__global__ void __launch_bounds__(CH_THREADS)
-k_enc_tables2(const float* __restrict__ raw, int M, int K, int dist, const uint8_t* __restrict__ images, int W,
-              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
-              int32_t* trace_cdf) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    EncTabSmem& S = *reinterpret_cast<EncTabSmem*>(smem_raw);
-    load_consts(&S.cc);
-    if (threadIdx.x < KMAX) S.zero[threadIdx.x] = 0.0f;
-    const int tid = threadIdx.x;
-    for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
-        const int64_t img = g / N, nn = g - img * N;
-        __syncthreads();                                  // previous pixel's tables are done with S.raw/params
-        for (int m = tid; m < M; m += CH_THREADS) S.raw[m] = __ldg(raw + g * M + m);
-        __syncthreads();
-        if (tid < K) {
-            const int i = tid;
-#pragma unroll 1
-            for (int ch = 0; ch < 3; ch++) {
-                S.pi[ch][i] = mix_pi(S.raw, K, ch, i);
-                S.inv[ch][i] = mix_inv(S.raw, K, ch, i);
-                S.mu0[ch][i] = S.raw[3 * K + ch * K + i];
-            }
-            S.ta[i] = tanhf_glibc(S.raw[9 * K + i]);
-            S.tb[i] = tanhf_glibc(S.raw[10 * K + i]);
-            S.tc[i] = tanhf_glibc(S.raw[11 * K + i]);
-        }
-        const int32_t ij = __ldg(order + nn);
-        const uint8_t* px = images + ((int64_t)img * N + (int64_t)(ij >> 16) * W + (ij & 0xFFFF)) * 3;
-        const int s0 = __ldg(px), s1 = __ldg(px + 1), s2 = __ldg(px + 2);
-        const float rn = S.cc.lut[s0], gn = S.cc.lut[s1];
-        __syncthreads();
-        int32_t* tr = trace_cdf ? trace_cdf + g * 3 * 257 : nullptr;
-        int sym;
-        uint32_t st0, ms0, st1, ms1, st2, ms2;
-        chain_table<KU, false>(S.pi[0], S.inv[0], S.mu0[0], S.zero, nullptr, 0.0f, 0.0f, K, dist, &S.cc, &S.ch, 0u,
-                               sym, st0, ms0, tr, s0);
-        chain_table<KU, false>(S.pi[1], S.inv[1], S.mu0[1], S.ta, nullptr, rn, 0.0f, K, dist, &S.cc, &S.ch, 0u, sym,
-                               st1, ms1, tr ? tr + 257 : nullptr, s1);
-        chain_table<KU, true>(S.pi[2], S.inv[2], S.mu0[2], S.tb, S.tc, rn, gn, K, dist, &S.cc, &S.ch, 0u, sym, st2,
-                              ms2, tr ? tr + 514 : nullptr, s2);
-        if (tid == 0) {
-            sw[g * 3 + 0] = (st0 << 16) | (ms0 - 1);
-            sw[g * 3 + 1] = (st1 << 16) | (ms1 - 1);
-            sw[g * 3 + 2] = (st2 << 16) | (ms2 - 1);
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // range coder (coder.py:30-73 + the encoder loop, codec.py:178-183), in

@@ -114,6 +114,21 @@ struct RcDecoder {
             range <<= 8;
         }
     }
+    // The same, branch-free (so it can be scheduled into the shadow of other
+    // work): r >= 2^24 and width >= 1 bound the renormalisation to two bytes.
+    __device__ __forceinline__ void advance_bf(uint64_t r, uint32_t start, uint32_t width) {
+        code -= r * start;
+        const uint64_t rg = r * width;
+        const bool n1 = rg < RC_BOTTOM, n2 = rg < (RC_BOTTOM >> 8);
+        const bool in0 = pos < len, in1 = pos + 1 < len;
+        const uint64_t b0 = (n1 && in0) ? (uint64_t)__ldg(data + pos) : 0ull;
+        const uint64_t b1 = (n2 && in1) ? (uint64_t)__ldg(data + pos + 1) : 0ull;
+        virt += (int)(n1 && !in0) + (int)(n2 && !in1);        // bytes past the end read as 0
+        status |= virt > 3 ? ST_CORRUPT : 0;                 // coder.py:94-95
+        code = n2 ? (((code << 16) & RC_MASK) | (b0 << 8) | b1) : (n1 ? (((code << 8) & RC_MASK) | b0) : code);
+        range = n2 ? rg << 16 : (n1 ? rg << 8 : rg);
+        pos += (int64_t)n1 + (int64_t)n2;
+    }
 };
 
 // RangeDecoder with a prefetched byte window: the decoder chain (lpic_decode.cuh)
