@@ -277,21 +277,28 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
                 f[4 * K + q] = tanhf_glibc(myraw[11 * K + q]);
             }
             *reinterpret_cast<int32_t*>(f + 5 * K) = (i << 16) | j;
+            __threadfence();
         }
-        // red tables: warp w builds the tables of pixels w, w+8, ...
+        __syncthreads();
+        // red tables, one warp per pixel (pixels w, w+8, ...); each record is
+        // published as soon as its table is written, so the consumer can start
+        // on the first pixels of a chunk before its last table is built
         for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
+            const float* myraw = rawbuf + p * P.w.MP;
+            const int64_t np_ = (int64_t)n0 + p;
+            unsigned char* rec = ring + (int64_t)(np_ & (P.ring_size - 1)) * P.rec_bytes;
             uint32_t start[8], mass[8];
-            if (P.f32) warp_table32(rawbuf + p * P.w.MP, K, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
-            else warp_table(rawbuf + p * P.w.MP, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
-            unsigned char* rec = ring + (int64_t)((n0 + p) & (P.ring_size - 1)) * P.rec_bytes;
+            if (P.f32) warp_table32(myraw, K, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
+            else warp_table(myraw, K, P.dist, 0, 0.0f, 0.0f, cc, sc + wid, start, mass);
             uint4 v;
             v.x = (start[0] & 0xFFFFu) | (start[1] << 16); v.y = (start[2] & 0xFFFFu) | (start[3] << 16);
             v.z = (start[4] & 0xFFFFu) | (start[5] << 16); v.w = (start[6] & 0xFFFFu) | (start[7] << 16);
             reinterpret_cast<uint4*>(rec)[lane] = v;
+            __threadfence();                                  // this lane's record bytes, device-wide
+            __syncwarp();
+            if (lane == 0) st_release_u32(flags + (np_ & (P.ring_size - 1)), (uint32_t)(np_ + 1));
         }
-        __threadfence();
-        __syncthreads();
-        if (act) st_release_u32(flags + (n & (P.ring_size - 1)), (uint32_t)(n + 1));
+        __syncthreads();                                      // (raw / activation buffers are reused next chunk)
         if (dbg && tid == 0) dbg[3] = gtimer();
     }
     if (P.fast) {
