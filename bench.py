@@ -49,6 +49,14 @@ CONFIGS = {
 }
 
 
+# DRAM bytes (read + write) per k_decode2 launch from one `ncu --set full`
+# capture of the same workload (algorithmic: ~2 B per sub-pixel = image byte +
+# payload; the rest is the L2-resident record ring spilling to DRAM)
+NCU_TRAFFIC = {
+    ("c2", "compat", False): (64194560 + 28143872, "profiles/r1_sweep3/ncu_dec_c2_raw.csv"),
+}
+
+
 def make_images(cfgd, rank: int, world: int, gray: bool):
     """(images (n,H,W,3) u8, description) for this rank.  Weak scaling: every
     rank codes its own images (seeds rank*n ...).  c4 (strong): one 8192^2
@@ -355,7 +363,9 @@ def run_ours(args, cfgd):
             "e2e": {"value": e2e_dec, "unit": unit, "h2d_bytes_per_step": int(lens.sum()) + 16 * n,
                     "d2h_bytes_per_step": int(3 * N * n) + 4 * n},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_tflops"],
-                         "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"], "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"],
+                         "traffic": NCU_TRAFFIC.get((args.config, args.precision, args.gray), (None, None))[0],
+                         "traffic_source": NCU_TRAFFIC.get((args.config, args.precision, args.gray), (None, None))[1],
                          "peak_kind": peak_kind,
                          "note": "model FLOPs (38,912/sub-pixel) per decode; the decoder is bound by the serial "
                                  "per-stream range-coder chain, see DESIGN.md"},

@@ -160,6 +160,12 @@ int main() {
     {
         long long h32[2]; cudaMemcpy(h32, d, 16, cudaMemcpyDeviceToHost);
         printf("chain_table K=3 FAST(f32): %lld cycles per table\n", h32[0]);
+#ifdef PROF
+        long long hp[16]; cudaMemcpyFromSymbol(hp, g_prof, sizeof(hp));
+        const char* nm[14] = {"P cdf", "bar E", "pmf+fx", "bar T", "Q rest", "bar A", "S level2+", "prefix", "-",
+                              "D search", "Q scale", "P z", "P phi", "S level1"};
+        for (int i = 0; i < 14; i++) printf("  f32 %-10s %6lld cycles/table\n", nm[i], hp[i] / 4000);
+#endif
     }
     k_time<false><<<1, NTH>>>(4000, d);
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
