@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out) {
+__global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out, double inv_scale = 1.0) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ __align__(16) CSM cs;
     __shared__ double pi[4], inv[4];
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out) {
     if (threadIdx.x < 16) s_prof[threadIdx.x] = 0;
 #endif
     if (threadIdx.x < 3) {
-        pi[threadIdx.x] = 0.3 + 0.05 * threadIdx.x; inv[threadIdx.x] = 1.1 + 0.2 * threadIdx.x;
+        pi[threadIdx.x] = 0.3 + 0.05 * threadIdx.x; inv[threadIdx.x] = (1.1 + 0.2 * threadIdx.x) * inv_scale;
         mu0[threadIdx.x] = 0.1f * threadIdx.x - 0.1f; ta[threadIdx.x] = 0.5f; tb[threadIdx.x] = -0.3f;
     }
     __syncthreads();
@@ -170,6 +170,16 @@ int main() {
     k_time<false><<<1, NTH>>>(4000, d);
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("chain_table K=3: %lld cycles per table (%s)\n", h[0], cudaGetErrorString(cudaGetLastError()));
+#ifndef PROF
+    {   // near-flat mixtures (s ~ e^7): most remainders share the first digit
+        k_time<false><<<1, NTH>>>(2000, d, 0.001);
+        long long hf[2]; cudaMemcpy(hf, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 flat: %lld cycles per table\n", hf[0]);
+        k_time<false><<<1, NTH>>>(2000, d, 0.02);
+        cudaMemcpy(hf, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 wide: %lld cycles per table\n", hf[0]);
+    }
+#endif
 #ifdef PROF
     long long hp[16]; cudaMemcpyFromSymbol(hp, g_prof, sizeof(hp));
     const char* nm[14] = {"P cdf", "bar E", "pmf+fx", "bar T", "Q rest", "bar A", "S level2+", "prefix", "-", "D search",
