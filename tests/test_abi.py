@@ -61,3 +61,15 @@ def test_no_cpu_fallback_without_cuda():
         P.encode(np.zeros((4, 4, 3), np.uint8), w, cfg, "wave")
     with pytest.raises(NativeUnavailable):
         P.forward_full(np.zeros((4, 4, 3), np.float32), w, cfg)
+
+
+def test_status_and_precision_constants_match_header():
+    """The Python layer's status / precision codes equal the header's #defines."""
+    from paper_2212_01185_b200 import _native
+    src = open(os.path.join(ROOT, "include", "lpic_b200.h")).read()
+    defs = dict(re.findall(r"#define\s+(LPIC_[SP][A-Z_]*)\s+(\d+)", src))
+    for name in ("LPIC_S_OK", "LPIC_S_NONFINITE", "LPIC_S_CORRUPT", "LPIC_S_CAPACITY", "LPIC_S_INTERNAL"):
+        assert name in defs, name
+        if hasattr(_native, name):
+            assert getattr(_native, name) == int(defs[name]), name
+    assert int(defs["LPIC_PREC_COMPAT"]) == 0 and int(defs["LPIC_PREC_FAST"]) == 1

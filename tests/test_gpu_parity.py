@@ -375,3 +375,35 @@ def test_gpu_two_streams_per_cluster(P, oracle_mod):
         assert np.array_equal(a, b)
     ow = oracle_weights(oracle_mod, w, cfg)
     assert conts[0].payload == oracle_mod.encode(ow, imgs[0], "wave")
+
+
+@pytest.mark.gpu
+def test_gpu_encoder_chase_matches_serial_plan(P):
+    """The encoder's range-coder plan normally chases the table kernel on a
+    side stream; LPIC_NO_CHASE=1 runs it after the tables.  Both must give
+    the same payload bytes (checked in a child process, since the switch is
+    read once per process), including a batch large enough for the serial
+    fallback (> 64 streams)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, hashlib, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "import paper_2212_01185_b200 as P\n"
+        "from paper_2212_01185_b200 import synth\n"
+        "w, cfg = synth.baseline_weights()\n"
+        "h = hashlib.sha256()\n"
+        "for n, H, W in ((3, 48, 40), (70, 16, 24)):\n"
+        "    rng = np.random.default_rng(n)\n"
+        "    imgs = [rng.integers(0, 256, (H, W, 3), dtype=np.uint8) for _ in range(n)]\n"
+        "    for c in P.encode_batch(imgs, w, cfg, 'wave'):\n"
+        "        h.update(c.to_bytes())\n"
+        "print(h.hexdigest())\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_extra in ({}, {"LPIC_NO_CHASE": "1"}):
+        env = dict(os.environ, **env_extra)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
