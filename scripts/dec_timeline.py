@@ -7,6 +7,8 @@ from paper_2212_01185_b200 import _native, synth
 H = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 W = int(sys.argv[2]) if len(sys.argv) > 2 else H
 NI = int(sys.argv[3]) if len(sys.argv) > 3 else 1      # streams decoded concurrently (stream 0 is traced)
+if os.environ.get("LPIC_PRECISION"):
+    P.set_precision(os.environ["LPIC_PRECISION"])     # compat (default) or fast
 w, cfg = synth.baseline_weights()
 imgs = synth.batch(NI, H, W)
 cs = P.encode_batch(imgs, w, cfg, "wave")
