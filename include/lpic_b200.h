@@ -131,6 +131,12 @@ int lpic_theoretical_bits(lpic_model_t* m, const uint8_t* d_images, int n, int H
                           void* stream);
 /* number of kernel launches issued by the last codec call (for bench accounting) */
 int lpic_last_launch_count(const lpic_model_t* m);
+/* training._mixture_loss (training.py:138-213), teacher forced, float64:
+ * d_raw (N, 12K) f32 network outputs, d_images (N, 3) u8 -> d_logp (N) f64
+ * = sum over r, g, b of log P(sub-pixel) (loss = -sum(d_logp) / (N ln 2)),
+ * and, if d_draw is not null, d loss / d raw (N, 12K) f32. */
+int lpic_mixture_loss_grad(const float* d_raw, const uint8_t* d_images, int64_t N, int K, int dist, double* d_logp,
+                           float* d_draw, void* stream);
 
 #ifdef __cplusplus
 }

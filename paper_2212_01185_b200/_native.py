@@ -33,6 +33,7 @@ EXPORTS = (
     "lpic_forward_full", "lpic_channel_cdfs", "lpic_rc_encode_streams", "lpic_rc_decode_tables",
     "lpic_encode_batch_device", "lpic_decode_batch_device", "lpic_encode_batch", "lpic_decode_batch",
     "lpic_last_launch_count", "lpic_true_symbol_probs", "lpic_theoretical_bits", "lpic_network_coding_order",
+    "lpic_mixture_loss_grad",
 )
 
 
@@ -79,6 +80,7 @@ def load(path: str = LIB_PATH):
     L.lpic_true_symbol_probs.argtypes = [_vp, _i64, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]
     L.lpic_theoretical_bits.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_network_coding_order.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
+    L.lpic_mixture_loss_grad.argtypes = [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]
     _lib = L
     return L
 

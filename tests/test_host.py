@@ -217,3 +217,20 @@ def test_gray_helpers():
     assert rgb.shape == (16, 20, 3) and np.array_equal(rgb[:, :, 1], g)
     with pytest.raises(ValueError):
         P.gray_to_rgb(rgb)
+
+
+def test_training_api_mirrors_reference():
+    """The GPU trainer exposes the reference trainer's names and config
+    fields (training.py:34-60, 219-333) and refuses to run without CUDA."""
+    import dataclasses
+    from paper_2212_01185_b200 import training
+    for name in ("TrainConfig", "GradientSet", "zero_gradients", "learning_rate", "loss", "backward", "Adam",
+                 "EpochStats", "train", "write_curve"):
+        assert hasattr(training, name), name
+    fields = [f.name for f in dataclasses.fields(training.TrainConfig)]
+    assert fields == ["batch_size", "crop", "lr", "lr_decay", "lr_decay_every", "epochs", "seed", "beta1", "beta2",
+                      "eps"]
+    tc = training.TrainConfig(lr=1e-3, lr_decay=0.5, lr_decay_every=2)
+    assert training.learning_rate(tc, 0) == 1e-3 and training.learning_rate(tc, 5) == 1e-3 * 0.25
+    with pytest.raises(ValueError):
+        training.TrainConfig(lr=0.0)
