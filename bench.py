@@ -170,6 +170,8 @@ def run_reference(args, cfgd):
     if rank != 0:
         return
     w, cfg = synth.baseline_weights()
+    if args.weights == "fitted":             # (the same fitted weights as our arm; fitting is not timed)
+        w, cfg, _ = synth.fitted_weights()
     n, H, W = cfgd["n"], cfgd["H"], cfgd["W"]
     threads = os.cpu_count() or 1
     imgs = make_images(cfgd, 0, 1, args.gray)[:threads]
@@ -187,7 +189,7 @@ def run_reference(args, cfgd):
         "metric": "decode Msubpixel/s (wavefront)", "value": value, "unit": "Msubpixel/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
-        "data": "synthetic", "config": {"workload": cfgd["desc"], "mode": args.mode, "weights": "kaiming seed 0"},
+        "data": "synthetic", "config": {"workload": cfgd["desc"], "mode": args.mode, "weights": "kaiming seed 0" + (" fitted 200 steps" if args.weights == "fitted" else "")},
         "cpu_baseline": {"value": value, "unit": "Msubpixel/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "Msubpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -212,6 +214,9 @@ def run_ours(args, cfgd):
     dev = torch.device("cuda", local)
     L = _native.require_cuda()
     w, cfg = synth.baseline_weights()
+    fit_curve = None
+    if args.weights == "fitted":
+        w, cfg, fit_curve = synth.fitted_weights()
     H, W = cfgd["H"], cfgd["W"]
     N = H * W
     mode = P.parse_mode(args.mode)
@@ -354,7 +359,9 @@ def run_ours(args, cfgd):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"] + (" -- grayscale variant" if args.gray else ""),
                        "images_per_gpu": n, "mode": args.mode,
-                       "weights": "kaiming seed 0 (K=3,C=128,L=5,h=2)",
+                       "weights": ("kaiming seed 0 (K=3,C=128,L=5,h=2)" if args.weights == "kaiming" else
+                                   "kaiming seed 0 fitted 200 steps on the GPU trainer (K=3,C=128,L=5,h=2), "
+                                   f"final train loss {fit_curve[-1].loss_bits_per_pixel / 3:.3f} bpsp"),
                        "precision": ("compat (bit-exact fp32 net)" if args.precision == "compat"
                                      else "fast (tcgen05 fp16x3 net)"),
                        "l2": "256 MiB flush between timed steps"},
@@ -408,6 +415,8 @@ def main():
     ap.add_argument("--sample-px", type=int, default=12288)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weights", default="kaiming", choices=["kaiming", "fitted"],
+                    help="BASELINE configs[1]: Kaiming seed 0, optionally fitted for 200 trainer steps")
     ap.add_argument("--gray", action="store_true", help="grayscale variant (r=g=b replication, BASELINE configs[4])")
     ap.add_argument("--precision", default="compat", choices=["compat", "fast"],
                     help="compat: reference-exact fp32 network (default); fast: tcgen05 fp16x3 network")

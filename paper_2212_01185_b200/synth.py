@@ -72,3 +72,17 @@ def synth_1f_gray(seed: int, H: int, W: int, beta=None, sigma=None, contrast: fl
     x = (x - x.mean()) / (x.std() + 1e-12)
     img = x * contrast + 128.0 + rng.standard_normal((H, W)) * sigma
     return np.clip(np.rint(img), 0, 255).astype(np.uint8)
+
+
+def fitted_weights(steps: int = 200, seed: int = 0, n_train: int = 64, size: int = 128):
+    """BASELINE configs[1]'s optional variant: Kaiming seed 0 weights fitted
+    for `steps` steps of the trainer (TrainConfig defaults: batch 64 of 64x64
+    crops, Adam lr 1e-4 with its stepped decay) on images of the same 1/f
+    generator (seeds 10_000.. -- disjoint from the benchmark images).  Runs on
+    the GPU (training.py); deterministic for a given device and library."""
+    from . import training
+    w, cfg = baseline_weights()
+    imgs = list(batch(n_train, size, size, seed0=10_000 + 1000 * seed))
+    tc = training.TrainConfig(batch_size=n_train, epochs=steps, seed=seed)   # one batch per epoch
+    w, curve = training.train(imgs, tc, cfg, initial=w)
+    return w, cfg, curve
