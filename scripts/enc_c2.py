@@ -7,6 +7,8 @@ from paper_2212_01185_b200 import _native, synth
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 H, W = 512, 768
 w, cfg = synth.baseline_weights()
+if os.environ.get("FITTED"):
+    w, cfg, _ = synth.fitted_weights()
 imgs = synth.batch(n, H, W)
 cs = P.encode_batch(imgs, w, cfg, "wave")
 if "--decode" in sys.argv:
