@@ -1,13 +1,18 @@
 // lpic_kernels.cu -- B200 (sm_100a) kernels and the C-ABI of liblpic_b200.so.
 //
 // Kernels (see DESIGN.md for rooflines):
-//   k_encode     fused encoder: causal gather -> network -> 3 quantised CDF
-//                tables per pixel -> packed (start,width) in coding order
-//                (codec.py:116-183, kernels.py:88-114, 296-313)
-//   k_rc_encode  one range-coder lane (warp) per stream (coder.py:30-73)
-//   k_decode2    wavefront decoder, one 2-CTA cluster per stream
-//                (producer + serial chain, lpic_decode.cuh; codec.py:193-247)
-//   k_forward_taps / k_channel_cdfs / k_rc_decode_tables  parity seams
+//   k_enc_net / k_enc_net_tc   encoder network over 64/128-pixel tiles in
+//                              coding order (compat CUDA cores / FAST tcgen05)
+//                              (codec.py:116-145, kernels.py:88-114)
+//   k_enc_tables<VAR,BIG>      three quantised CDF tables per pixel -> the
+//                              coded symbols' (start, width) (kernels.py:296-313)
+//   k_rc_plan / k_rc_chunks / k_rc_merge
+//                              parallel byte-exact range coder (coder.py:30-73);
+//                              the plan chases the table kernel on a side stream
+//   k_decode2                  wavefront decoder, one 2-CTA cluster per stream
+//                              (producer + serial chain, lpic_decode.cuh;
+//                              codec.py:193-247)
+//   k_forward_taps / k_channel_cdfs / k_rc_decode_tables / k_true_*   parity seams
 #include "../../include/lpic_b200.h"
 
 #include <cuda_runtime.h>
@@ -84,7 +89,7 @@ template <int CP, int HH>
 __global__ void __launch_bounds__(NT_THREADS)
 k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, const int32_t* __restrict__ order,
           int64_t N, float* __restrict__ raw_out, int32_t* status, float* trace_raw) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     constexpr int TC = Taps<HH>::TC;
     __shared__ float lut[256];
     float* fb = reinterpret_cast<float*>(smem);
@@ -502,43 +507,6 @@ k_rc_merge(const int64_t* __restrict__ off, const int64_t* __restrict__ cnt, int
     lens[s] = S + 3;
 }
 
-// Legacy sequential lane (kept for the explicit-stream parity entry point)
-__global__ void __launch_bounds__(32)
-k_rc_encode(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
-            int64_t fixed_cnt, uint8_t* out, int64_t cap_each, int64_t* lens, int32_t* status) {
-    __shared__ uint32_t sbuf[RC_CHUNK];
-    const int s = blockIdx.x, lane = threadIdx.x;
-    const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
-    const int64_t n = cnt ? cnt[s] : fixed_cnt;
-    const uint32_t* p = sw + base;
-    RcEncoder e;
-    e.init(out + (int64_t)s * cap_each, cap_each);
-    uint32_t nxt[RC_CHUNK / 32];
-    bool no_wait = false;
-    rc_sym_load(p, n, 0, lane, nxt, false, no_wait);
-    for (int64_t c = 0; c < n; c += RC_CHUNK) {
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
-        __syncwarp();
-        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt, false, no_wait);
-        if (lane == 0) {
-            const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
-            uint32_t x = sbuf[0];
-#pragma unroll 1
-            for (int k = 0; k < m; k++) {
-                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
-                e.encode(x >> 16, (x & 0xFFFFu) + 1u, true);
-                x = y;
-            }
-        }
-    }
-    if (lane == 0) {
-        const int64_t len = e.finish(true);
-        lens[s] = len;
-        if (e.status) atomicOr(status + s, e.status);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // unquantised probability of the realised bin (kernels.true_symbol_probs,
@@ -603,7 +571,7 @@ k_true_bits(const float* __restrict__ raw, int M, int K, int dist, const uint8_t
 template <int CP, int HH>
 __global__ void __launch_bounds__(NET_THREADS)
 k_forward_taps(NetDev w, const float* __restrict__ taps, int64_t N, float* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     float* raw = reinterpret_cast<float*>(smem);
     float* zbuf = raw + NET_THREADS * w.MP;
     const int64_t n = (int64_t)blockIdx.x * NET_THREADS + threadIdx.x;
@@ -619,7 +587,7 @@ k_forward_taps(NetDev w, const float* __restrict__ taps, int64_t N, float* __res
 template <int CP, int HH>
 __global__ void __launch_bounds__(NET_THREADS)
 k_forward_full(NetDev w, const float* __restrict__ plane, int H, int W, float* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     float* raw = reinterpret_cast<float*>(smem);
     float* zbuf = raw + NET_THREADS * w.MP;
     const int64_t n = (int64_t)blockIdx.x * NET_THREADS + threadIdx.x;
