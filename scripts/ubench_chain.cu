@@ -14,6 +14,7 @@ __shared__ long long s_prof[16];     // shared accumulator: no global latency in
 #define LPIC_CHAIN_PROF s_prof
 #endif
 #include "lpic_chain.cuh"
+#include "lpic_rc.cuh"
 using namespace lpic;
 #define CT chain_table
 #define CSM ChainSmem
@@ -99,8 +100,14 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
     }
 }
 
-template <bool F32>
-__global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out, double inv_scale = 1.0) {
+// spin_warps > 0: that many extra warps poll shared memory with nanosleep
+// while the chain runs (the decoder's loader and publisher warps do that)
+template <bool F32, bool DEC = false>
+__global__ void __launch_bounds__(NTH + 64, 1) k_time(int tables, long long* out, double inv_scale = 1.0,
+                                                      int spin_ns = 0, const uint8_t* payload = nullptr,
+                                                      int64_t plen = 0) {
+    __shared__ volatile int stop;
+    __shared__ volatile unsigned long long sink;
     __shared__ __align__(16) CdfConsts cc;
     __shared__ __align__(16) CSM cs;
     __shared__ double pi[4], inv[4];
@@ -113,19 +120,38 @@ __global__ void __launch_bounds__(NTH, 1) k_time(int tables, long long* out, dou
         pi[threadIdx.x] = 0.3 + 0.05 * threadIdx.x; inv[threadIdx.x] = (1.1 + 0.2 * threadIdx.x) * inv_scale;
         mu0[threadIdx.x] = 0.1f * threadIdx.x - 0.1f; ta[threadIdx.x] = 0.5f; tb[threadIdx.x] = -0.3f;
     }
+    if (threadIdx.x == 0) { stop = 0; sink = 0; }
     __syncthreads();
+    if (threadIdx.x >= NTH) {                        // spinner warps
+        if ((threadIdx.x & 31) == 0) {
+            unsigned long long x = 0;
+            while (!stop) { __nanosleep(spin_ns); x += sink + 1; }
+            sink = x;
+        }
+        return;
+    }
     long long t0 = clock64();
     uint32_t acc = 0;
     uint32_t target = 1234;
+    RcDecoder dec;
+    if (DEC) dec.init(payload, plen);
+    uint64_t r = 0;
+    uint32_t p_st = 0, p_ms = 1;
     for (int it = 0; it < tables; it++) {
         const float rn = -1.0f + 0.001f * (it & 1023);
         int sym; uint32_t st, ms;
-        CT<3, true, F32>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
+        if constexpr (DEC) {        // the decoder's deferred advance + target, as in dec_consumer
+            auto tgt = [&]() { dec.advance_bf(r, p_st, p_ms); return dec.target(r); };
+            CT<3, true, F32>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, tgt, sym, st, ms, nullptr);
+            p_st = st; p_ms = ms;
+        } else {
+            CT<3, true, F32>(pi, inv, mu0, ta, tb, rn, 0.25f, 3, 0, &cc, &cs, target, sym, st, ms, nullptr);
+        }
         acc += st + ms;
         target = (target * 2654435761u + st) & 0xFFFFu;     // dependency on the previous result
     }
     long long t1 = clock64();
-    if (threadIdx.x == 0) { out[0] = (t1 - t0) / tables; out[1] = acc; }
+    if (threadIdx.x == 0) { out[0] = (t1 - t0) / tables; out[1] = acc; stop = 1; }
 #ifdef PROF
     if (threadIdx.x < 16) g_prof[threadIdx.x] = s_prof[threadIdx.x];
 #endif
@@ -171,6 +197,20 @@ int main() {
     long long h[2]; cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("chain_table K=3: %lld cycles per table (%s)\n", h[0], cudaGetErrorString(cudaGetLastError()));
 #ifndef PROF
+    {   // with the range decoder's deferred advance/target inside the table (as in the decoder)
+        uint8_t* pl; cudaMalloc(&pl, 1 << 20);
+        cudaMemset(pl, 0x5A, 1 << 20);
+        k_time<false, true><<<1, NTH>>>(4000, d, 1.0, 0, pl, 1 << 20);
+        long long hs[2]; cudaMemcpy(hs, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 with decoder advance/target: %lld cycles per table (%s)\n", hs[0],
+               cudaGetErrorString(cudaGetLastError()));
+        cudaFree(pl);
+    }
+    for (int ns : {32, 256}) {   // with two polling warps beside the chain (as in the decoder)
+        k_time<false><<<1, NTH + 64>>>(4000, d, 1.0, ns);
+        long long hs[2]; cudaMemcpy(hs, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 with 2 polling warps (nanosleep %d): %lld cycles per table\n", ns, hs[0]);
+    }
     {   // near-flat mixtures (s ~ e^7): most remainders share the first digit
         k_time<false><<<1, NTH>>>(2000, d, 0.001);
         long long hf[2]; cudaMemcpy(hf, d, 16, cudaMemcpyDeviceToHost);
