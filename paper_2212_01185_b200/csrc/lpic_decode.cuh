@@ -322,7 +322,7 @@ struct ConsumerSmem {
 };
 
 template <int KU, int NT, bool F32>
-__device__ __noinline__ void dec_consumer(const DecParams& P, int img0, unsigned char* smem) {
+__device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsigned char* smem) {
     CdfConsts* cc = reinterpret_cast<CdfConsts*>(smem);
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * P.rec_bytes;
     unsigned char* gbase = smem + ((sizeof(CdfConsts) + 127) & ~(size_t)127);
