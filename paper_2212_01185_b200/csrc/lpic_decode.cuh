@@ -173,7 +173,11 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     // FAST precision: the tensor-core tile state and a raw buffer replace the fp32 tile buffers
     const size_t tc_off = dec_fbase_off();
     TcSmem* tcs = reinterpret_cast<TcSmem*>(smem + tc_off);
-    float* fraw = reinterpret_cast<float*>(smem + tc_off + sizeof(TcSmem));
+    // (the raw outputs reuse the A-operand buffer: the last layer's epilogue
+    // writes them after its MMAs completed, and the next tile's input is
+    // stored only after this chunk's records and tables have read them;
+    // 64 x MP floats <= 32 KB since FAST needs 12K <= 128)
+    float* fraw = reinterpret_cast<float*>(tcs->a_hi);
     uint32_t mcnt = 0;
     load_consts(cc);
     if (P.fast && threadIdx.x < 128) tc_init(tcs);

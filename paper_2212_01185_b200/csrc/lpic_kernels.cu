@@ -923,7 +923,7 @@ int decode_geometry(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
 
 size_t dec_smem_bytes(int CP, int TC, int MT, int MP, int rec_bytes, int S, bool fast) {
     const size_t prod = fast ? dec_fbase_off() +
-                                   sizeof(TcSmem) + (size_t)NT_TP * MP * 4
+                                   sizeof(TcSmem)
                              : dec_fbase_off() + net_tile_floats(CP, TC, MT, MP) * 4;
     const size_t grp = ((sizeof(ConsumerSmem) + 127) & ~(size_t)127) + (size_t)DEC_SLOTS * rec_bytes;
     const size_t cons = ((sizeof(CdfConsts) + 127) & ~(size_t)127) + (size_t)S * grp;

@@ -459,3 +459,45 @@ def test_gpu_training_run_tracks_reference(P):
     for n, t in zip(_TRAIN_NAMES, w.tensors()):
         exp = g[f"run_w_{n}"]
         assert float(np.abs(t - exp).max()) <= 1e-3 * float(np.abs(exp).max()) + 1e-9, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,dist", [(11, 0), (16, 1), (5, 0)])
+def test_gpu_many_mixtures_match_oracle(P, oracle_mod, K, dist):
+    """Mixture counts beyond the fast paths: K = 11 and 16 take the encoder's
+    one-channel-at-a-time table kernel (3K > 32) and the decoder's runtime-K
+    chain; K = 5 the generic compile-time path.  Payloads byte-identical to
+    the C oracle, lossless round trip (ModelConfig allows K <= 16 on device)."""
+    from paper_2212_01185_b200 import synth
+    from paper_2212_01185_b200.network import Distribution, ModelConfig, glorot_weights
+    cfg = ModelConfig(mixtures=K, filters=16, layers=4, distribution=Distribution(dist))
+    w = glorot_weights(cfg, np.random.default_rng(K))
+    imgs = synth.batch(2, 13, 17, seed0=300 + K)
+    cs = P.encode_batch(imgs, w, cfg, "wave")
+    ow = oracle_weights(oracle_mod, w, cfg)
+    assert [c.payload for c in cs] == oracle_mod.encode_batch(ow, imgs, "wave")
+    for a, b in zip(P.decode_batch(cs, w, cfg), imgs):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_gpu_fast_many_mixtures(P):
+    """FAST precision at the edge of its tensor-core tile: K = 10 (M = 120
+    outputs) round-trips losslessly; K = 11 (M = 132) is refused loudly
+    (LpicError), never silently run on another path."""
+    from paper_2212_01185_b200 import synth
+    from paper_2212_01185_b200.errors import LpicError
+    from paper_2212_01185_b200.network import ModelConfig, glorot_weights
+    imgs = synth.batch(2, 13, 17, seed0=500)
+    P.set_precision("fast")
+    try:
+        cfg = ModelConfig(mixtures=10, filters=16, layers=4)
+        w = glorot_weights(cfg, np.random.default_rng(10))
+        outs = P.decode_batch(P.encode_batch(imgs, w, cfg, "wave"), w, cfg)
+        for a, b in zip(outs, imgs):
+            assert np.array_equal(a, b)
+        cfg11 = ModelConfig(mixtures=11, filters=16, layers=4)
+        with pytest.raises(LpicError):
+            P.encode_batch(imgs, glorot_weights(cfg11, np.random.default_rng(11)), cfg11, "wave")
+    finally:
+        P.set_precision("compat")
