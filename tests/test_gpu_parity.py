@@ -501,3 +501,47 @@ def test_gpu_fast_many_mixtures(P):
             P.encode_batch(imgs, glorot_weights(cfg11, np.random.default_rng(11)), cfg11, "wave")
     finally:
         P.set_precision("compat")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C,h,modes", [(32, 3, ("seq", "wave")), (48, 2, ("wave", "diag")), (64, 1, ("seq", "wave"))])
+def test_gpu_filter_and_kernel_sizes_match_oracle(P, oracle_mod, C, h, modes):
+    """The padded-filter instantiations (CP = 32, 64; C = 48 pads to 64) and
+    kernel half-widths 1 and 3 (72-value causal context): payloads
+    byte-identical to the C oracle, lossless round trip, in every mode the
+    reference allows for h (diagonal is h = 2 only)."""
+    from paper_2212_01185_b200 import synth
+    from paper_2212_01185_b200.network import ModelConfig, glorot_weights
+    cfg = ModelConfig(mixtures=3, filters=C, layers=5, kernel_half=h)
+    w = glorot_weights(cfg, np.random.default_rng(C + h))
+    imgs = synth.batch(2, 19, 23, seed0=700 + C)
+    ow = oracle_weights(oracle_mod, w, cfg)
+    for mode in modes:
+        cs = P.encode_batch(imgs, w, cfg, mode)
+        assert [c.payload for c in cs] == oracle_mod.encode_batch(ow, imgs, mode), mode
+        for a, b in zip(P.decode_batch(cs, w, cfg), imgs):
+            assert np.array_equal(a, b), mode
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C,h", [(32, 3), (64, 1), (128, 3)])
+def test_gpu_fast_filter_and_kernel_sizes_roundtrip(P, C, h):
+    """FAST (tcgen05) network with other K/N paddings: h = 3 (72 inputs),
+    h = 1 (12 inputs), C = 32 / 64 / 128: lossless round trip and bpsp within
+    0.5% of the compat (reference-exact) stream."""
+    from paper_2212_01185_b200 import synth
+    from paper_2212_01185_b200.network import ModelConfig, glorot_weights
+    cfg = ModelConfig(mixtures=3, filters=C, layers=5, kernel_half=h)
+    w = glorot_weights(cfg, np.random.default_rng(C * 10 + h))
+    imgs = synth.batch(2, 24, 20, seed0=900 + C)
+    ref = sum(len(c.payload) for c in P.encode_batch(imgs, w, cfg, "wave"))
+    P.set_precision("fast")
+    try:
+        cs = P.encode_batch(imgs, w, cfg, "wave")
+        outs = P.decode_batch(cs, w, cfg)
+    finally:
+        P.set_precision("compat")
+    for a, b in zip(outs, imgs):
+        assert np.array_equal(a, b)
+    got = sum(len(c.payload) for c in cs)
+    assert abs(got - ref) <= 0.005 * ref + 8, (got, ref)
