@@ -190,6 +190,12 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
     // the red tables' selection histograms (8 warps x 1 KB) live in a buffer
     // that is idle between the network and the next chunk's gather
     WarpCdfScratch* sc = P.fast ? reinterpret_cast<WarpCdfScratch*>(tcs->a_lo) : reinterpret_cast<WarpCdfScratch*>(nb.act0);
+    // red-table warps: all of the CTA's warps when the scratch region holds
+    // one histogram per warp (act0 + act1 span >= 64 KB... i.e. CP >= 32; FAST: a_lo, 32 KB)
+    const int tab_warps = (int)(blockDim.x >> 5) > 8 &&
+                                  (P.fast || (size_t)((CP > Taps<HH>::TC ? CP : Taps<HH>::TC) + CP) * NT_TP * 4 >=
+                                                 (blockDim.x >> 5) * sizeof(WarpCdfScratch))
+                              ? (int)(blockDim.x >> 5) : 8;
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int K = P.K;
     const int64_t N = P.N;
@@ -287,7 +293,7 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
         // red tables, one warp per pixel (pixels w, w+8, ...); each record is
         // published as soon as its table is written, so the consumer can start
         // on the first pixels of a chunk before its last table is built
-        for (int p = wid; wid < 8 && p < npx; p += 8) {      // (warps >= 8 only join the barriers)
+        for (int p = wid; wid < tab_warps && p < npx; p += tab_warps) {   // (other warps only join the barriers)
             const float* myraw = rawbuf + p * P.w.MP;
             const int64_t np_ = (int64_t)n0 + p;
             unsigned char* rec = ring + (int64_t)(np_ & (P.ring_size - 1)) * P.rec_bytes;
