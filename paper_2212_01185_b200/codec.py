@@ -157,7 +157,7 @@ def encode(image: np.ndarray, w: Weights, cfg: ModelConfig, mode, trace: CodecTr
     _check_mode(mode, cfg)
     H, W, _ = image.shape
     payload = _encode_group(image[None], w, cfg, mode, trace)[0]
-    return Container(mode, cfg.mixtures, int(cfg.distribution), W, H, network.weight_fingerprint(w, cfg), payload)
+    return Container(mode, cfg.mixtures, int(cfg.distribution), W, H, network.container_fingerprint(w, cfg), payload)
 
 
 def encode_batch(images, w: Weights, cfg: ModelConfig, mode) -> list:
@@ -168,7 +168,7 @@ def encode_batch(images, w: Weights, cfg: ModelConfig, mode) -> list:
     images = list(images) if not isinstance(images, np.ndarray) or images.ndim != 4 else list(images)
     for im in images:
         _check_image(im)
-    fp = network.weight_fingerprint(w, cfg)
+    fp = network.container_fingerprint(w, cfg)
     out: list = [None] * len(images)
     groups: dict = {}
     for k, im in enumerate(images):
@@ -182,6 +182,10 @@ def encode_batch(images, w: Weights, cfg: ModelConfig, mode) -> list:
 
 def _check_container(container: Container, w: Weights, cfg: ModelConfig, fp: int) -> None:
     if container.weight_fingerprint != fp:
+        other = "fast" if network.get_precision() == "compat" else "compat"
+        if container.weight_fingerprint == network.container_fingerprint(w, cfg, other):
+            raise FingerprintMismatchError(
+                f"container was encoded in {other} precision; decode it with set_precision({other!r})")
         raise FingerprintMismatchError("container was encoded with different weights")
     if container.mixtures != cfg.mixtures or container.distribution != int(cfg.distribution):
         raise LpicError("container model header does not match the config")
@@ -230,7 +234,7 @@ def _decode_group(conts: list, w: Weights, cfg: ModelConfig, trace: CodecTrace |
 def decode(container: Container, w: Weights, cfg: ModelConfig, trace: CodecTrace | None = None) -> np.ndarray:
     """Reconstruct the exact image from a container on the GPU."""
     network.check_weights(w, cfg)
-    _check_container(container, w, cfg, network.weight_fingerprint(w, cfg))
+    _check_container(container, w, cfg, network.container_fingerprint(w, cfg))
     return _decode_group([container], w, cfg, trace)[0]
 
 
@@ -238,7 +242,7 @@ def decode_batch(containers, w: Weights, cfg: ModelConfig) -> list:
     """Decode many containers; same-geometry streams share one launch (one
     CTA per stream)."""
     network.check_weights(w, cfg)
-    fp = network.weight_fingerprint(w, cfg)
+    fp = network.container_fingerprint(w, cfg)
     containers = list(containers)
     for c in containers:
         _check_container(c, w, cfg, fp)

@@ -101,6 +101,8 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// one acquire after a relaxed poll succeeded (instead of an acquiring poll)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_volatile_smem(const volatile uint32_t* p) { return *p; }
 __device__ __forceinline__ unsigned long long ld_volatile_smem64(const unsigned long long* p) {
     return *reinterpret_cast<const volatile unsigned long long*>(p);
@@ -239,6 +241,10 @@ __device__ void dec_producer(const DecParams& P, int img, unsigned char* smem) {
             const int64_t need = s_need;
             uint32_t ns = 32;
             while ((int64_t)ld_relaxed_u32(progress) < need) { __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+            // acquire: the publisher's st.release of `progress` now happens-before
+            // this thread's later operations, and the barrier below extends that
+            // to every thread's gather of the decoded pixels
+            fence_acq_rel_gpu();
             if (dbg) dbg[1] = gtimer();
         }
         __syncthreads();
@@ -380,6 +386,9 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
                 const uint32_t* fl = flags + (n & (P.ring_size - 1));
                 uint32_t ns = 32;
                 while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { publish(n); __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+                // acquire (pairs with the producer's st.release of the flag), then
+                // order the generic-proxy view before the bulk copy's async proxy
+                fence_acq_rel_gpu();
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 mbar_arrive_tx(&cs->full[s], (uint32_t)P.rec_bytes);
                 bulk_g2s(slots + s * P.rec_bytes, ring + (int64_t)(n & (P.ring_size - 1)) * P.rec_bytes,

@@ -8,7 +8,8 @@
 //                              coded symbols' (start, width) (kernels.py:296-313)
 //   k_rc_plan / k_rc_chunks / k_rc_merge
 //                              parallel byte-exact range coder (coder.py:30-73);
-//                              the plan chases the table kernel on a side stream
+//                              the plan is fused into the table kernel's
+//                              cooperative launch (it chases the symbols)
 //   k_decode2                  wavefront decoder, one 2-CTA cluster per stream
 //                              (producer + serial chain, lpic_decode.cuh;
 //                              codec.py:193-247)
@@ -185,6 +186,136 @@ k_enc_net_tc(const __grid_constant__ TcNetDev w, const uint8_t* __restrict__ ima
     tc_finish(s);
 }
 
+constexpr int RC_CH = 1024;
+constexpr int RC_CHUNK = 256;
+static_assert(RC_CH % RC_CHUNK == 0 && (RC_CH & (RC_CH - 1)) == 0, "chunk boundaries on block starts");
+
+constexpr uint32_t RC_PENDING = 0xFFFFFFFFu;    // sw sentinel: start 65535 + width 65536 cannot occur
+constexpr unsigned long long RC_STALL_NS = 4000000000ull;   // chase: no new symbol for 4 s -> give up
+__device__ __forceinline__ uint32_t ld_relaxed_sw(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sw(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long rc_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// chase: the symbols are still being produced (by the table warps of the same
+// cooperative launch); wait for each until it is no longer RC_PENDING.  The
+// wait is bounded by wall time without progress; once it trips, every later
+// load is a plain load (no further waiting).
+__device__ __forceinline__ void rc_sym_load(const uint32_t* __restrict__ p, int64_t n, int64_t c, int lane,
+                                            uint32_t (&nxt)[RC_CHUNK / 32], bool chase, bool& timed_out) {
+#pragma unroll
+    for (int q = 0; q < RC_CHUNK / 32; q++) {
+        const int64_t k = c + 32 * q + lane;
+        nxt[q] = (k < n) ? (chase ? ld_relaxed_sw(p + k) : __ldg(p + k)) : 0u;
+    }
+    if (chase) {
+        bool pend = false;
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) pend |= (c + 32 * q + lane < n) && nxt[q] == RC_PENDING;
+        if (!__any_sync(0xffffffffu, pend)) return;
+        unsigned long long t0 = rc_gtimer();
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) {
+            const int64_t k = c + 32 * q + lane;
+            while (k < n && nxt[q] == RC_PENDING && !timed_out) {
+                __nanosleep(128);
+                nxt[q] = ld_relaxed_sw(p + k);
+                if (nxt[q] != RC_PENDING) t0 = rc_gtimer();
+                else if (rc_gtimer() - t0 > RC_STALL_NS) timed_out = true;
+            }
+        }
+        timed_out = __any_sync(0xffffffffu, timed_out);
+    }
+}
+
+// The serial part of the parallel range coder for one stream, run by one
+// warp: the range sequence range_{i+1} = norm((range_i >> 16) * width_i)
+// (coder.py:37-57, widths only), recording range and byte position at every
+// RC_CH-symbol chunk boundary.  sbuf: RC_CHUNK words of warp-private shared
+// memory.  Returns false if a chased symbol never arrived.
+__device__ __forceinline__ bool rc_plan_stream(const uint32_t* __restrict__ p, int64_t n, uint32_t* sbuf,
+                                               unsigned long long* __restrict__ R_out, int64_t* __restrict__ P_out,
+                                               bool chase) {
+    const int lane = threadIdx.x & 31;
+    uint32_t nxt[RC_CHUNK / 32];
+    bool timed_out = false;
+    rc_sym_load(p, n, 0, lane, nxt, chase, timed_out);
+    uint64_t R = RC_TOP - 1;
+    int64_t S = 0;
+    for (int64_t c = 0; c < n; c += RC_CHUNK) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
+        __syncwarp();
+        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt, chase && !timed_out, timed_out);
+        if (lane == 0) {
+            if ((c & (RC_CH - 1)) == 0) { R_out[c / RC_CH] = R; P_out[c / RC_CH] = S; }   // RC_CH % RC_CHUNK == 0
+            const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
+            uint32_t r = (uint32_t)(R >> 16);
+            uint32_t x = sbuf[0];
+            uint32_t sb = 0;                                   // shifts in this block
+#pragma unroll 4
+            for (int k = 0; k < m; k++) {
+                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
+                // range' = r * width; renormalise by whole bytes (sh <= 2 as
+                // r >= 2^24): next r = (range' << 8sh) >> 16.  The three
+                // candidate shifts are formed in parallel and selected, so the
+                // serial chain is multiply -> shift -> two selects.
+                const uint32_t wq = (x & 0xFFFFu) + 1u;
+                const uint32_t hi = __umulhi(r, wq), lo = r * wq;     // 32-bit halves: 32-bit compares
+                const uint32_t r16 = __funnelshift_r(lo, hi, 16), r8 = __funnelshift_r(lo, hi, 8);
+                sb += (hi < 0x100u) + (hi == 0u);
+                r = hi >= 0x100u ? r16 : (hi != 0u ? r8 : lo);
+                x = y;
+            }
+            S += sb;
+            R = (uint64_t)r << 16;      // only r = R >> 16 matters to the next symbol
+        }
+    }
+    if (lane == 0) P_out[(n + RC_CH - 1) / RC_CH] = S;
+    return !timed_out;
+}
+
+// Stand-alone plan (after the tables, or over explicit streams): one warp
+// per stream, RC_PLAN_WARPS streams per block.
+constexpr int RC_PLAN_WARPS = 4;
+__global__ void __launch_bounds__(32 * RC_PLAN_WARPS)
+k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
+          int64_t fixed_cnt, int max_chunks, unsigned long long* __restrict__ Rc, int64_t* __restrict__ posc,
+          int n_streams) {
+    __shared__ uint32_t sbuf_all[RC_PLAN_WARPS][RC_CHUNK];
+    const int s = blockIdx.x * RC_PLAN_WARPS + (threadIdx.x >> 5);
+    if (s >= n_streams) return;
+    const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
+    const int64_t n = cnt ? cnt[s] : fixed_cnt;
+    rc_plan_stream(sw + base, n, sbuf_all[threadIdx.x >> 5], Rc + (int64_t)s * max_chunks,
+                   posc + (int64_t)s * (max_chunks + 1), false);
+}
+
+// The plan run INSIDE the table kernel (fused encoder): warp 0 of blocks
+// [0, n_plan) follows streams blockIdx.x, blockIdx.x + n_plan, ... while the
+// other warps of the same cooperative launch produce the symbols.  A
+// cooperative launch guarantees every block is resident, so the chase cannot
+// wait on a block that never runs (whatever else shares the GPU, and under
+// tools that serialise kernels).
+struct RcPlanArgs {
+    int n_plan;                        // blocks whose warp 0 runs the plan (0 = none)
+    int n_streams;
+    int max_chunks;
+    int64_t count;                     // symbols per stream
+    unsigned long long* Rc;
+    int64_t* posc;
+    int32_t* status;
+};
+
 // ---------------------------------------------------------------------------
 // encoder, stage 2: three quantised CDF tables per pixel (warp builder) and
 // the coded symbol's (start, width) in coding order (codec.py:168-182)
@@ -198,7 +329,7 @@ template <int VAR, bool BIG>
 __global__ void __launch_bounds__(TAB_WARPS * 32)
 k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
-             int32_t* trace_cdf, unsigned long long* __restrict__ ctr) {
+             int32_t* trace_cdf, unsigned long long* __restrict__ ctr, const RcPlanArgs plan) {
     constexpr bool f32 = VAR == 2;
     constexpr int dist = VAR == 1 ? 1 : 0;
     __shared__ __align__(16) CdfConsts cc;
@@ -207,6 +338,18 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
     load_consts(&cc);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (wid == 0 && (int)blockIdx.x < plan.n_plan) {
+        // range-coder plan warp: chase this block's streams (warp 0's
+        // histogram scratch is its symbol buffer)
+        bool ok = true;
+        for (int s = blockIdx.x; s < plan.n_streams; s += plan.n_plan) {
+            ok = rc_plan_stream(sw + (int64_t)s * plan.count, plan.count, sc[0].hist,
+                                plan.Rc + (int64_t)s * plan.max_chunks, plan.posc + (int64_t)s * (plan.max_chunks + 1),
+                                ok) && ok;
+            if (!ok && lane == 0) atomicOr(plan.status + s, LPIC_S_INTERNAL);
+        }
+        return;
+    }
     // work item t -> pixel nn = t / nimg of image t % nimg: every image's
     // symbols complete front to back at the same rate, which the chasing
     // range-coder plan (k_rc_plan, chase mode) follows
@@ -246,7 +389,7 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
                     uint32_t st = 0, ms = 1;
 #pragma unroll
                     for (int q = 0; q < 8; q++) if (q == (sym & 7)) { st = start[q]; ms = mass[q]; }
-                    sw[g * 3 + ch] = (st << 16) | (ms - 1);
+                    st_relaxed_sw(sw + g * 3 + ch, (st << 16) | (ms - 1));
                 }
                 if (trace_cdf) store_cdf_row(trace_cdf + (g * 3 + ch) * 257, start, mass);
             }
@@ -276,7 +419,7 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
                 uint32_t st = 0, ms = 1;
 #pragma unroll
                 for (int q = 0; q < 8; q++) if (q == (sym & 7)) { st = start[q]; ms = mass[q]; }
-                sw[g * 3 + ch] = (st << 16) | (ms - 1);
+                st_relaxed_sw(sw + g * 3 + ch, (st << 16) | (ms - 1));
             }
             if (trace_cdf) store_cdf_row(trace_cdf + (g * 3 + ch) * 257, start, mass);
         }
@@ -285,29 +428,52 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
     }
 }
 
-template <int VAR>
-void launch_enc_tables_v(bool big, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
-                         const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
-                         unsigned long long* ctr, cudaStream_t st) {
-    if (big) k_enc_tables<VAR, true><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc, ctr);
-    else k_enc_tables<VAR, false><<<g, TAB_WARPS * 32, 0, st>>>(raw, M, K, images, W, order, N, total, sw, tc, ctr);
+template <int VAR, bool BIG>
+cudaError_t launch_enc_tables_vb(int64_t blocks, int sms, const float* raw, int M, int K, const uint8_t* images,
+                                 int W, const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
+                                 unsigned long long* ctr, RcPlanArgs plan, cudaStream_t st) {
+    auto kern = k_enc_tables<VAR, BIG>;
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TAB_WARPS * 32, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    // persistent grid (work is grabbed from a global counter): every block resident
+    int64_t g = (int64_t)occ * sms;
+    if (plan.n_plan > 0) {
+        if (plan.n_plan > g / 2) plan.n_plan = (int)(g / 2);
+        if (plan.n_plan < 1) plan.n_plan = 0;
+        g = g < blocks + plan.n_plan ? g : blocks + plan.n_plan;
+    } else {
+        g = g < blocks ? g : blocks;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(TAB_WARPS * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = plan.n_plan > 0 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, raw, M, K, images, W, order, N, total, sw, tc, ctr, plan);
 }
-int preload_enc_tables(int var, int K) {
+// Launch the table kernel; with plan.n_plan > 0 as ONE cooperative launch
+// whose plan warps chase the symbols.  Returns the error of the launch (a
+// cooperative launch can be refused, e.g. when the GPU is partitioned).
+cudaError_t launch_enc_tables(int var, int64_t blocks, int sms, const float* raw, int M, int K, const uint8_t* images,
+                              int W, const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
+                              unsigned long long* ctr, const RcPlanArgs& plan, cudaStream_t st) {
     const bool big = 3 * K > 32;
-    cudaFuncAttributes fa;
-    cudaError_t e;
-    if (var == 2) e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<2, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<2, false>);
-    else if (var == 1) e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<1, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<1, false>);
-    else e = big ? cudaFuncGetAttributes(&fa, k_enc_tables<0, true>) : cudaFuncGetAttributes(&fa, k_enc_tables<0, false>);
-    return e == cudaSuccess ? 0 : fail(LPIC_E_CUDA, cudaGetErrorString(e));
-}
-void launch_enc_tables(int var, unsigned g, const float* raw, int M, int K, const uint8_t* images, int W,
-                       const int32_t* order, int64_t N, int64_t total, uint32_t* sw, int32_t* tc,
-                       unsigned long long* ctr, cudaStream_t st) {
-    const bool big = 3 * K > 32;
-    if (var == 2) launch_enc_tables_v<2>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
-    else if (var == 1) launch_enc_tables_v<1>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
-    else launch_enc_tables_v<0>(big, g, raw, M, K, images, W, order, N, total, sw, tc, ctr, st);
+#define LPIC_TAB(v)                                                                                                  \
+    return big ? launch_enc_tables_vb<v, true>(blocks, sms, raw, M, K, images, W, order, N, total, sw, tc, ctr, plan, \
+                                               st)                                                                   \
+               : launch_enc_tables_vb<v, false>(blocks, sms, raw, M, K, images, W, order, N, total, sw, tc, ctr,    \
+                                                plan, st);
+    if (var == 2) { LPIC_TAB(2) }
+    if (var == 1) { LPIC_TAB(1) }
+    LPIC_TAB(0)
+#undef LPIC_TAB
 }
 
 
@@ -331,95 +497,6 @@ void launch_enc_tables(int var, unsigned g, const float* raw, int M, int K, cons
 //   3. k_rc_merge  one lane per stream adds every chunk's window and carry-outs
 //                  (rare ripples through 0xFF runs) and applies finish().
 // ---------------------------------------------------------------------------
-constexpr int RC_CH = 1024;
-constexpr int RC_CHUNK = 256;
-static_assert(RC_CH % RC_CHUNK == 0 && (RC_CH & (RC_CH - 1)) == 0, "chunk boundaries on block starts");
-
-constexpr uint32_t RC_PENDING = 0xFFFFFFFFu;    // sw sentinel: start 65535 + width 65536 cannot occur
-__device__ __forceinline__ uint32_t ld_relaxed_sw(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-// chase: the symbols are still being produced (k_enc_tables on another
-// stream); wait for each until it is no longer RC_PENDING
-__device__ __forceinline__ void rc_sym_load(const uint32_t* __restrict__ p, int64_t n, int64_t c, int lane,
-                                            uint32_t (&nxt)[RC_CHUNK / 32], bool chase, bool& timed_out) {
-#pragma unroll
-    for (int q = 0; q < RC_CHUNK / 32; q++) {
-        const int64_t k = c + 32 * q + lane;
-        nxt[q] = (k < n) ? (chase ? ld_relaxed_sw(p + k) : __ldg(p + k)) : 0u;
-    }
-    if (chase) {
-#pragma unroll
-        for (int q = 0; q < RC_CHUNK / 32; q++) {
-            const int64_t k = c + 32 * q + lane;
-            uint32_t spins = 0;                       // (bounded: a failed producer must not hang the device)
-            while (k < n && nxt[q] == RC_PENDING) {
-                if (++spins > (1u << 26)) { timed_out = true; break; }
-                __nanosleep(256);
-                nxt[q] = ld_relaxed_sw(p + k);
-            }
-        }
-    }
-}
-
-// RC_PLAN_WARPS streams per block, one warp each (one per SM sub-partition);
-// in chase mode the block also claims most of the SM's shared memory so no
-// table block shares its SM: the serial chains then issue undisturbed.
-constexpr int RC_PLAN_WARPS = 4;
-__global__ void __launch_bounds__(32 * RC_PLAN_WARPS)
-k_rc_plan(const uint32_t* __restrict__ sw, const int64_t* __restrict__ off, const int64_t* __restrict__ cnt,
-          int64_t fixed_cnt, int max_chunks, unsigned long long* __restrict__ Rc, int64_t* __restrict__ posc,
-          int chase, int32_t* status, int n_streams) {
-    __shared__ uint32_t sbuf_all[RC_PLAN_WARPS][RC_CHUNK];
-    const int s = blockIdx.x * RC_PLAN_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (s >= n_streams) return;
-    uint32_t* sbuf = sbuf_all[threadIdx.x >> 5];
-    const int64_t base = off ? off[s] : (int64_t)s * fixed_cnt;
-    const int64_t n = cnt ? cnt[s] : fixed_cnt;
-    const uint32_t* p = sw + base;
-    unsigned long long* R_out = Rc + (int64_t)s * max_chunks;
-    int64_t* P_out = posc + (int64_t)s * (max_chunks + 1);
-    uint32_t nxt[RC_CHUNK / 32];
-    bool timed_out = false;
-    rc_sym_load(p, n, 0, lane, nxt, chase != 0, timed_out);
-    uint64_t R = RC_TOP - 1;
-    int64_t S = 0;
-    for (int64_t c = 0; c < n; c += RC_CHUNK) {
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < RC_CHUNK / 32; q++) sbuf[32 * q + lane] = nxt[q];
-        __syncwarp();
-        rc_sym_load(p, n, c + RC_CHUNK, lane, nxt, chase != 0 && !timed_out, timed_out);
-        if (lane == 0) {
-            if ((c & (RC_CH - 1)) == 0) { R_out[c / RC_CH] = R; P_out[c / RC_CH] = S; }   // RC_CH % RC_CHUNK == 0
-            const int m = (int)((n - c) < RC_CHUNK ? (n - c) : RC_CHUNK);
-            uint32_t r = (uint32_t)(R >> 16);
-            uint32_t x = sbuf[0];
-            uint32_t sb = 0;                                   // shifts in this block
-#pragma unroll 4
-            for (int k = 0; k < m; k++) {
-                const uint32_t y = sbuf[(k + 1) & (RC_CHUNK - 1)];
-                // range' = r * width; renormalise by whole bytes (sh <= 2 as
-                // r >= 2^24): next r = (range' << 8sh) >> 16.  The three
-                // candidate shifts are formed in parallel and selected, so the
-                // serial chain is multiply -> shift -> two selects.
-                const uint32_t wq = (x & 0xFFFFu) + 1u;
-                const uint32_t hi = __umulhi(r, wq), lo = r * wq;     // 32-bit halves: 32-bit compares
-                const uint32_t r16 = __funnelshift_r(lo, hi, 16), r8 = __funnelshift_r(lo, hi, 8);
-                sb += (hi < 0x100u) + (hi == 0u);
-                r = hi >= 0x100u ? r16 : (hi != 0u ? r8 : lo);
-                x = y;
-            }
-            S += sb;
-            R = (uint64_t)r << 16;      // only r = R >> 16 matters to the next symbol
-        }
-    }
-    if (lane == 0) P_out[(n + RC_CH - 1) / RC_CH] = S;
-    if (timed_out && status) atomicOr(status + s, LPIC_S_INTERNAL);
-}
-
 // carry of +1 into byte j, rippling back over 0xFF down to `floor`; returns 1
 // if it ran past `floor` (a carry out of the region)
 __device__ __forceinline__ int rc_carry_into(uint8_t* out, int64_t j, int64_t floor) {
@@ -689,11 +766,7 @@ struct lpic_model {
     uint32_t* d_flags = nullptr; size_t flags_cap = 0;
     uint32_t* d_progress = nullptr; size_t progress_cap = 0;
     unsigned long long* d_dbg = nullptr;   // optional decoder timeline (lpic_decode_debug)
-    // encoder: side stream (high priority) for the chasing range-coder plan
-    cudaStream_t side = nullptr;
     unsigned long long* d_ctr = nullptr;   // k_enc_tables work counter
-    bool enc_loaded = false;               // encoder kernels preloaded (chase mode)
-    cudaEvent_t ev_sw = nullptr, ev_plan = nullptr;
     int launches = 0;
     std::mutex mu;
 };
@@ -723,13 +796,9 @@ int rc_max_chunks(int64_t max_count) {
     return (int)((max_count + RC_CH - 1) / RC_CH) > 0 ? (int)((max_count + RC_CH - 1) / RC_CH) : 1;
 }
 int rc_plan(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt, int64_t fixed_cnt,
-            int n, int64_t max_count, bool chase, int32_t* d_status, cudaStream_t st) {
-    // chase: ~200 KB of (unused) dynamic shared memory reserves the SM
-    const int hog = chase ? 200 * 1024 : 0;
-    if (chase && cudaFuncSetAttribute(k_rc_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, hog) != cudaSuccess)
-        return fail(LPIC_E_CUDA, "k_rc_plan smem attribute");
-    k_rc_plan<<<(n + RC_PLAN_WARPS - 1) / RC_PLAN_WARPS, 32 * RC_PLAN_WARPS, hog, st>>>(
-        d_sw, d_off, d_cnt, fixed_cnt, rc_max_chunks(max_count), wk.R, wk.P, chase ? 1 : 0, d_status, n);
+            int n, int64_t max_count, cudaStream_t st) {
+    k_rc_plan<<<(n + RC_PLAN_WARPS - 1) / RC_PLAN_WARPS, 32 * RC_PLAN_WARPS, 0, st>>>(
+        d_sw, d_off, d_cnt, fixed_cnt, rc_max_chunks(max_count), wk.R, wk.P, n);
     CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -750,7 +819,7 @@ int rc_encode_finish(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_of
 int rc_encode_parallel(const RcWork& wk, const uint32_t* d_sw, const int64_t* d_off, const int64_t* d_cnt,
                        int64_t fixed_cnt, int n, int64_t max_count, uint8_t* d_out, int64_t cap_each,
                        int64_t* d_lens, int32_t* d_status, cudaStream_t st) {
-    if (int r = rc_plan(wk, d_sw, d_off, d_cnt, fixed_cnt, n, max_count, false, d_status, st)) return r;
+    if (int r = rc_plan(wk, d_sw, d_off, d_cnt, fixed_cnt, n, max_count, st)) return r;
     return rc_encode_finish(wk, d_sw, d_off, d_cnt, fixed_cnt, n, max_count, d_out, cap_each, d_lens, d_status, st);
 }
 
@@ -807,46 +876,25 @@ int launch_enc_net_tc(lpic_model* m, const uint8_t* d_images, int n, int H, int 
     return 0;
 }
 
-// The range-coder plan runs CONCURRENTLY with the table kernel: it is
-// launched on the model's high-priority side stream, follows each image's
-// symbols as they complete (RC_PENDING sentinels) and so finishes right after
-// the last table instead of adding its serial ~1.2 M-symbol chain afterwards.
-struct RcChase {
+// Encoder pipeline: network -> tables (+ the range-coder plan fused into the
+// same cooperative launch for <= RC_FUSED_MAX streams) -> chunks -> merge.
+// The plan's serial width chain then hides under the table work instead of
+// following it.  With more streams, or if the cooperative launch is refused,
+// the plan runs after the tables (k_rc_plan; it is then short next to them).
+constexpr int RC_FUSED_MAX = 64;
+struct RcPlanWork {
     RcWork wk;
     int64_t count;               // symbols per stream (3N)
 };
 
 template <int CP, int HH> struct EncodeRun {
+    // *fused_out: 1 if the plan ran inside the table launch
     static int run(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw, uint32_t* sw,
-                   int32_t* d_status, float* tr, int32_t* tc, const RcChase* chase, cudaStream_t st) {
+                   int32_t* d_status, float* tr, int32_t* tc, const RcPlanWork& pw, int* fused_out, cudaStream_t st) {
         constexpr int TC = Taps<HH>::TC;
         const int64_t N = (int64_t)H * W;
         if (!m->d_ctr && cudaMalloc(&m->d_ctr, sizeof(unsigned long long)) != cudaSuccess)
             return fail(LPIC_E_NOMEM, "cudaMalloc work counter failed");
-        // chase: the plan goes first (before the network), so its blocks are
-        // resident before the table kernel's persistent blocks fill the GPU.
-        // Every kernel enqueued behind it is loaded first: under lazy module
-        // loading a first launch could otherwise wait behind the spinning plan.
-        if (chase && !m->enc_loaded) {
-            cudaFuncAttributes fa;
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_enc_net<CP, HH>));
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_enc_net_tc<HH>));
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_plan));
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_chunks));
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_rc_merge));
-            CUDA_TRY(cudaFuncGetAttributes(&fa, k_pack));
-            for (int var = 0; var < 3; var++)
-                if (int r = preload_enc_tables(var, m->K)) return r;
-            m->enc_loaded = true;
-        }
-        if (chase) {
-            CUDA_TRY(cudaMemsetAsync(sw, 0xFF, sizeof(uint32_t) * (size_t)N * n * 3, st));
-            CUDA_TRY(cudaEventRecord(m->ev_sw, st));
-            CUDA_TRY(cudaStreamWaitEvent(m->side, m->ev_sw, 0));
-            if (int r = rc_plan(chase->wk, sw, nullptr, nullptr, chase->count, n, chase->count, true, d_status, m->side))
-                return r;
-            CUDA_TRY(cudaEventRecord(m->ev_plan, m->side));
-        }
         if (m->precision == LPIC_PREC_FAST) {
             if (int r = launch_enc_net_tc<HH>(m, d_images, n, H, W, mode, raw, d_status, tr, st)) return r;
         } else {
@@ -860,11 +908,29 @@ template <int CP, int HH> struct EncodeRun {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
         const int64_t blocks = (total + TAB_WARPS - 1) / TAB_WARPS;
-        const unsigned g2 = (unsigned)(blocks < (int64_t)sms * 4 ? blocks : (int64_t)sms * 4);   // (dynamic work: >= resident)
+        const int var = (m->precision == LPIC_PREC_FAST && m->dist == 0) ? 2 : m->dist;
         CUDA_TRY(cudaMemsetAsync(m->d_ctr, 0, sizeof(unsigned long long), st));
-        launch_enc_tables((m->precision == LPIC_PREC_FAST && m->dist == 0) ? 2 : m->dist, g2, raw, m->M, m->K, d_images,
-                          W, m->d_order, N, total, sw, tc, m->d_ctr, st);
-        CUDA_TRY(cudaGetLastError());
+        RcPlanArgs plan{};
+        static const bool fuse_env = std::getenv("LPIC_RC_UNFUSED") == nullptr;   // (A/B timing only)
+        if (fuse_env && n <= RC_FUSED_MAX) {
+            CUDA_TRY(cudaMemsetAsync(sw, 0xFF, sizeof(uint32_t) * (size_t)N * n * 3, st));   // RC_PENDING
+            plan.n_plan = n;
+            plan.n_streams = n;
+            plan.max_chunks = rc_max_chunks(pw.count);
+            plan.count = pw.count;
+            plan.Rc = pw.wk.R;
+            plan.posc = pw.wk.P;
+            plan.status = d_status;
+            cudaError_t e = launch_enc_tables(var, blocks, sms, raw, m->M, m->K, d_images, W, m->d_order, N, total, sw,
+                                              tc, m->d_ctr, plan, st);
+            if (e == cudaSuccess) { *fused_out = 1; return 0; }
+            (void)cudaGetLastError();           // refused (e.g. partitioned GPU): unfused below
+            plan = RcPlanArgs{};
+        }
+        *fused_out = 0;
+        cudaError_t e = launch_enc_tables(var, blocks, sms, raw, m->M, m->K, d_images, W, m->d_order, N, total, sw, tc,
+                                          m->d_ctr, plan, st);
+        if (e != cudaSuccess) return fail(LPIC_E_CUDA, std::string("k_enc_tables: ") + cudaGetErrorString(e));
         return 0;
     }
 };
@@ -1156,9 +1222,6 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_rcR); cudaFree(m->d_rcW); cudaFree(m->d_rcP); cudaFree(m->d_rcC);
     cudaFree(m->d_tc);
     cudaFree(m->d_ctr);
-    if (m->ev_sw) cudaEventDestroy(m->ev_sw);
-    if (m->ev_plan) cudaEventDestroy(m->ev_plan);
-    if (m->side) cudaStreamDestroy(m->side);
     delete m;
     return 0;
 }
@@ -1218,14 +1281,24 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
     int64_t mx = 1;
     for (int64_t c : hc) mx = c > mx ? c : mx;
     const int64_t mc = (mx + RC_CH - 1) / RC_CH;
-    RcWork wk{};
-    CUDA_TRY(cudaMalloc(&wk.R, sizeof(unsigned long long) * n_streams * mc));
-    CUDA_TRY(cudaMalloc(&wk.W, sizeof(unsigned long long) * n_streams * mc));
-    CUDA_TRY(cudaMalloc(&wk.P, sizeof(int64_t) * n_streams * (mc + 1)));
-    CUDA_TRY(cudaMalloc(&wk.C, sizeof(int32_t) * n_streams * mc));
-    const int r = rc_encode_parallel(wk, d_sw, d_off, d_cnt, 0, n_streams, mx, d_out, cap_each, d_len, d_status, st);
-    cudaStreamSynchronize(st);
-    cudaFree(wk.R); cudaFree(wk.W); cudaFree(wk.P); cudaFree(wk.C);
+    // grow-only workspace shared by all calls (this entry point has no model handle)
+    static std::mutex ws_mu;
+    static RcWork ws{};
+    static size_t ws_cap = 0;     // chunk slots
+    std::lock_guard<std::mutex> lk(ws_mu);
+    const size_t need = (size_t)n_streams * (mc + 1);
+    if (need > ws_cap) {
+        cudaFree(ws.R); cudaFree(ws.W); cudaFree(ws.P); cudaFree(ws.C);
+        ws = RcWork{};
+        ws_cap = 0;
+        CUDA_TRY(cudaMalloc(&ws.R, sizeof(unsigned long long) * need));
+        CUDA_TRY(cudaMalloc(&ws.W, sizeof(unsigned long long) * need));
+        CUDA_TRY(cudaMalloc(&ws.P, sizeof(int64_t) * need));
+        CUDA_TRY(cudaMalloc(&ws.C, sizeof(int32_t) * need));
+        ws_cap = need;
+    }
+    const int r = rc_encode_parallel(ws, d_sw, d_off, d_cnt, 0, n_streams, mx, d_out, cap_each, d_len, d_status, st);
+    CUDA_TRY(cudaStreamSynchronize(st));      // (the workspace is reused by the next call)
     return r;
 }
 
@@ -1303,35 +1376,21 @@ int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, in
     if (int r = ensure(m->d_sw, m->sw_cap, (size_t)n * N * 3)) return r;
     if (int r = ensure(m->d_raw, m->raw_cap, (size_t)n * N * m->M)) return r;
     CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
-    if (!m->side) {                                   // created on first use (the library loads without a GPU)
-        int lo = 0, hi = 0;
-        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CUDA_TRY(cudaStreamCreateWithPriority(&m->side, cudaStreamNonBlocking, hi));
-        CUDA_TRY(cudaEventCreateWithFlags(&m->ev_sw, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&m->ev_plan, cudaEventDisableTiming));
-    }
     const int64_t mc = (3 * N + RC_CH - 1) / RC_CH;
     if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)n * mc)) return r;
     if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)n * mc)) return r;
     if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)n * (mc + 1))) return r;
     if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)n * mc)) return r;
-    const RcChase chase{RcWork{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC}, 3 * N};
-    // LPIC_NO_CHASE=1: plan after the tables on the caller's stream (for tools
-    // that serialise kernels, e.g. compute-sanitizer)
-    static const bool chase_env = std::getenv("LPIC_NO_CHASE") == nullptr;
-    const bool chase_on = chase_env && n <= 16 * RC_PLAN_WARPS;   // (larger batches: the plan is short next to the tables)
+    const RcPlanWork pw{RcWork{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC}, 3 * N};
+    int fused = 0;
     if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
-                                    d_trace_raw, d_trace_cdf, chase_on ? &chase : nullptr, st))
+                                    d_trace_raw, d_trace_cdf, pw, &fused, st))
         return r;
-    if (chase_on) {
-        CUDA_TRY(cudaStreamWaitEvent(st, m->ev_plan, 0));
-    } else if (int r = rc_plan(chase.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, false, d_status, st)) {
-        return r;
-    }
-    if (int r = rc_encode_finish(chase.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
+    if (!fused && (rc_plan(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, st))) return LPIC_E_CUDA;
+    if (int r = rc_encode_finish(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
                                  d_status, st))
         return r;
-    m->launches = 5;
+    m->launches = fused ? 4 : 5;
     return 0;
 }
 

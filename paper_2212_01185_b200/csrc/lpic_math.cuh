@@ -13,6 +13,16 @@
 //    update (/root/reference/pkg/src/lpic/kernels.py:234-241).
 //  * phi: the Gaussian / logistic CDF of kernels._cdf_value
 //    (/root/reference/pkg/src/lpic/kernels.py:202-209) in float64.
+//
+// expm1f_fdlibm / tanhf_glibc restate the algorithm, thresholds and
+// coefficients of fdlibm's s_expm1f.c and s_tanhf.c, which carry this notice:
+//
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this
+//   software is freely granted, provided that this notice
+//   is preserved.
 #pragma once
 #include <cstdint>
 

@@ -251,9 +251,16 @@ class GpuModel:
             pass
 
 
-_MODELS: dict = {}
+_MODELS: "OrderedDict" = None          # LRU of device handles (see gpu_model)
+MODEL_CACHE_SIZE = 4
 _PRECISION = {"compat": _native.PREC_COMPAT, "fast": _native.PREC_FAST}
 _precision = "compat"
+# FAST containers carry the weight fingerprint XOR this tag ("FAST" fp16x3),
+# so a FAST stream presented to a compat decoder -- this library in compat
+# precision or the CPU reference -- fails the fingerprint gate
+# (FingerprintMismatchError, codec.py:197-199 of the reference) instead of
+# silently decoding a wrong image, and vice versa.
+FAST_FINGERPRINT_TAG = 0x4641535466703136
 
 
 def set_precision(name: str) -> None:
@@ -263,8 +270,8 @@ def set_precision(name: str) -> None:
     parameters bit-identical to the CPU reference, streams interchangeable
     with it.  "fast": tcgen05 tensor-core GEMMs with the fp16x3 split (raw
     within ~1e-5 relative); such streams round-trip on this library only and
-    must be decoded with precision "fast" too (the container does not record
-    it, exactly as it does not record the weights beyond their fingerprint).
+    must be decoded with precision "fast" too.  FAST containers are tagged
+    (``container_fingerprint``) so any other decoder refuses them.
     """
     global _precision
     if name not in _PRECISION:
@@ -276,15 +283,42 @@ def get_precision() -> str:
     return _precision
 
 
+def container_fingerprint(w: Weights, cfg: ModelConfig, precision: str | None = None) -> int:
+    """The fingerprint written into (and required from) a container: the
+    weight fingerprint (network.py:264-281 of the reference) in compat
+    precision, tagged in FAST precision."""
+    fp = weight_fingerprint(w, cfg)
+    if (precision or _precision) == "fast":
+        fp ^= FAST_FINGERPRINT_TAG
+    return fp
+
+
 def gpu_model(w: Weights, cfg: ModelConfig) -> GpuModel:
+    """The device handle for (weights, config, device, precision), from a
+    small LRU: evicted handles free their device weights and workspaces."""
+    global _MODELS
     import torch
+    from collections import OrderedDict
     _native.require_cuda()
+    if _MODELS is None:
+        _MODELS = OrderedDict()
     key = (weight_fingerprint(w, cfg), cfg, torch.cuda.current_device(), _precision)
     m = _MODELS.get(key)
     if m is None:
         m = GpuModel(w, cfg, _PRECISION[_precision])
         _MODELS[key] = m
+        while len(_MODELS) > MODEL_CACHE_SIZE:
+            _MODELS.popitem(last=False)
+    else:
+        _MODELS.move_to_end(key)
     return m
+
+
+def release_models() -> None:
+    """Drop every cached device handle (frees their device memory once no
+    caller holds them)."""
+    if _MODELS is not None:
+        _MODELS.clear()
 
 
 def _kernel_call_taps(tap_values: np.ndarray, w: Weights, cfg: ModelConfig) -> np.ndarray:

@@ -378,12 +378,14 @@ def test_gpu_two_streams_per_cluster(P, oracle_mod):
 
 
 @pytest.mark.gpu
-def test_gpu_encoder_chase_matches_serial_plan(P):
-    """The encoder's range-coder plan normally chases the table kernel on a
-    side stream; LPIC_NO_CHASE=1 runs it after the tables.  Both must give
-    the same payload bytes (checked in a child process, since the switch is
-    read once per process), including a batch large enough for the serial
-    fallback (> 64 streams)."""
+def test_gpu_encoder_fused_plan_matches_serial_plan(P):
+    """The encoder's range-coder plan runs inside the table kernel's
+    cooperative launch (it chases the symbols); LPIC_RC_UNFUSED=1 runs it
+    after the tables.  Both must give the same payload bytes, and so must a
+    run with CUDA_LAUNCH_BLOCKING=1 (every launch serialised -- the case
+    that broke the round-1 side-stream chase), including a batch large
+    enough for the unfused path (> 64 streams).  Child processes, since the
+    switches are read once per process."""
     import subprocess
     import sys
     code = (
@@ -401,12 +403,38 @@ def test_gpu_encoder_chase_matches_serial_plan(P):
         "print(h.hexdigest())\n"
     ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for env_extra in ({}, {"LPIC_NO_CHASE": "1"}):
+    for env_extra in ({}, {"LPIC_RC_UNFUSED": "1"}, {"CUDA_LAUNCH_BLOCKING": "1"}):
         env = dict(os.environ, **env_extra)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2]
+
+
+@pytest.mark.gpu
+def test_gpu_fast_containers_are_tagged(P):
+    """FAST (tcgen05) streams must not decode silently in compat precision
+    or on the CPU reference: their container fingerprint is tagged, so the
+    fingerprint gate raises both ways (advice r1: silent corruption)."""
+    from paper_2212_01185_b200 import network, synth
+    w, cfg = synth.baseline_weights()
+    img = synth.synth_1f(3, 20, 24)
+    c_compat = P.encode(img, w, cfg, "wave")
+    assert c_compat.weight_fingerprint == P.weight_fingerprint(w, cfg)
+    P.set_precision("fast")
+    try:
+        c_fast = P.encode(img, w, cfg, "wave")
+        assert c_fast.weight_fingerprint == P.weight_fingerprint(w, cfg) ^ network.FAST_FINGERPRINT_TAG
+        assert np.array_equal(P.decode(c_fast, w, cfg), img)
+        with pytest.raises(P.FingerprintMismatchError, match="compat"):
+            P.decode(c_compat, w, cfg)
+    finally:
+        P.set_precision("compat")
+    with pytest.raises(P.FingerprintMismatchError, match="fast"):
+        P.decode(c_fast, w, cfg)
+    with pytest.raises(P.FingerprintMismatchError):
+        P.decode_batch([c_compat, c_fast], w, cfg)
+    assert np.array_equal(P.decode(c_compat, w, cfg), img)
 
 
 def _train_cfg(name):
