@@ -160,14 +160,54 @@ def encode(image: np.ndarray, w: Weights, cfg: ModelConfig, mode, trace: CodecTr
     return Container(mode, cfg.mixtures, int(cfg.distribution), W, H, network.container_fingerprint(w, cfg), payload)
 
 
-def encode_batch(images, w: Weights, cfg: ModelConfig, mode) -> list:
-    """Encode many images; same-size images share one batched launch."""
+def _on_devices(n: int, devices, fn) -> list:
+    """Run fn(lo, hi) -> list over contiguous slices of n items, one host
+    thread per device (shard.split_for_devices); the slices' results are
+    concatenated in order.  The C-ABI calls release the GIL, so the devices
+    work concurrently.  devices=None: the current device only."""
+    if devices is None or len(devices) <= 1:
+        if devices:
+            import torch
+            with torch.cuda.device(int(devices[0])):
+                return fn(0, n)
+        return fn(0, n)
+    import threading
+
+    import torch
+    from . import shard
+    parts = shard.split_for_devices(n, [int(d) for d in devices])
+    out: list = [None] * len(parts)
+    errs: list = []
+
+    def work(k, d, lo, hi):
+        try:
+            torch.cuda.set_device(d)
+            out[k] = fn(lo, hi)
+        except BaseException as e:        # re-raised on the caller's thread
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(k, d, lo, hi)) for k, (d, lo, hi) in enumerate(parts)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return [x for part in out for x in part]
+
+
+def encode_batch(images, w: Weights, cfg: ModelConfig, mode, devices=None) -> list:
+    """Encode many images; same-size images share one batched launch.
+    devices: optional list of CUDA device indices -- the batch is split into
+    contiguous slices, one per device, coded concurrently."""
     network.check_weights(w, cfg)
     mode = parse_mode(mode)
     _check_mode(mode, cfg)
-    images = list(images) if not isinstance(images, np.ndarray) or images.ndim != 4 else list(images)
+    images = list(images)
     for im in images:
         _check_image(im)
+    if devices:
+        return _on_devices(len(images), devices, lambda lo, hi: encode_batch(images[lo:hi], w, cfg, mode))
     fp = network.container_fingerprint(w, cfg)
     out: list = [None] * len(images)
     groups: dict = {}
@@ -238,14 +278,16 @@ def decode(container: Container, w: Weights, cfg: ModelConfig, trace: CodecTrace
     return _decode_group([container], w, cfg, trace)[0]
 
 
-def decode_batch(containers, w: Weights, cfg: ModelConfig) -> list:
+def decode_batch(containers, w: Weights, cfg: ModelConfig, devices=None) -> list:
     """Decode many containers; same-geometry streams share one launch (one
-    CTA per stream)."""
+    decoder cluster per stream).  devices: as in ``encode_batch``."""
     network.check_weights(w, cfg)
     fp = network.container_fingerprint(w, cfg)
     containers = list(containers)
     for c in containers:
         _check_container(c, w, cfg, fp)
+    if devices:
+        return _on_devices(len(containers), devices, lambda lo, hi: decode_batch(containers[lo:hi], w, cfg))
     out: list = [None] * len(containers)
     groups: dict = {}
     for k, c in enumerate(containers):

@@ -1064,6 +1064,17 @@ template <int CP, int HH> struct FullRun {
     }
 };
 
+// Every entry point that takes a model runs on the model's device and
+// restores the caller's current device (multi-device use from one thread).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != d && cudaSetDevice(d) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 int check_geom(const lpic_model* m, int n, int H, int W, int mode) {
     if (!m) return fail(LPIC_E_ARG, "null model");
     if (n < 0 || H < 1 || W < 1 || H > 32767 || W > 65535) return fail(LPIC_E_ARG, "bad image geometry");
@@ -1214,6 +1225,7 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
 
 int lpic_model_destroy(lpic_model_t* m) {
     if (!m) return 0;
+    DeviceGuard dg_(m->device);
     cudaFree(m->d_w);
     cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_raw); cudaFree(m->d_img); cudaFree(m->d_pay);
     cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
@@ -1250,12 +1262,14 @@ int lpic_decode_debug(lpic_model_t* m, unsigned long long* d_buf) {
 
 int lpic_forward_taps(lpic_model_t* m, const float* d_taps, int64_t N, float* d_raw, void* stream) {
     if (!m || N < 0) return fail(LPIC_E_ARG, "bad argument");
+    DeviceGuard dg_(m->device);
     if (N == 0) return 0;
     return dispatch<TapsRun>(m->CP, m->h, m, d_taps, N, d_raw, (cudaStream_t)stream);
 }
 
 int lpic_forward_full(lpic_model_t* m, const float* d_plane, int H, int W, float* d_raw, void* stream) {
     if (!m || H < 1 || W < 1) return fail(LPIC_E_ARG, "bad argument");
+    DeviceGuard dg_(m->device);
     return dispatch<FullRun>(m->CP, m->h, m, d_plane, H, W, d_raw, (cudaStream_t)stream);
 }
 
@@ -1283,9 +1297,14 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
     const int64_t mc = (mx + RC_CH - 1) / RC_CH;
     // grow-only workspace shared by all calls (this entry point has no model handle)
     static std::mutex ws_mu;
-    static RcWork ws{};
-    static size_t ws_cap = 0;     // chunk slots
+    static RcWork ws_dev[64] = {};
+    static size_t ws_cap_dev[64] = {};     // chunk slots, per device
     std::lock_guard<std::mutex> lk(ws_mu);
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(LPIC_E_UNSUPPORTED, "device index");
+    RcWork& ws = ws_dev[dev];
+    size_t& ws_cap = ws_cap_dev[dev];
     const size_t need = (size_t)n_streams * (mc + 1);
     if (need > ws_cap) {
         cudaFree(ws.R); cudaFree(ws.W); cudaFree(ws.P); cudaFree(ws.C);
@@ -1325,6 +1344,7 @@ int lpic_true_symbol_probs(const float* d_raw, int64_t N, int M, int K, int dist
 int lpic_network_coding_order(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, float* d_raw,
                               void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     std::lock_guard<std::mutex> lk(m->mu);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1347,6 +1367,7 @@ int lpic_network_coding_order(lpic_model_t* m, const uint8_t* d_images, int n, i
 int lpic_theoretical_bits(lpic_model_t* m, const uint8_t* d_images, int n, int H, int W, int mode, double* d_bits,
                           void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     std::lock_guard<std::mutex> lk(m->mu);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1368,29 +1389,48 @@ int lpic_encode_batch_device(lpic_model_t* m, const uint8_t* d_images, int n, in
                              uint8_t* d_payload, int64_t cap_each, int64_t* d_lens, int32_t* d_status,
                              float* d_trace_raw, int32_t* d_trace_cdf, void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     std::lock_guard<std::mutex> lk(m->mu);
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = (int64_t)H * W;
     if (int r = coding_order(m, H, W, mode, st)) return r;
-    if (int r = ensure(m->d_sw, m->sw_cap, (size_t)n * N * 3)) return r;
-    if (int r = ensure(m->d_raw, m->raw_cap, (size_t)n * N * m->M)) return r;
+    // The raw plane and the symbols are per-batch workspace: batches larger
+    // than the budget (LPIC_ENC_WORKSPACE_MB, default 4096) are encoded in
+    // image chunks, so any batch fits (BASELINE C3: 256 x 2048x1536 on one
+    // GPU would otherwise need ~116 GB of raw plane).
+    static const int64_t budget = [] {
+        const char* e = std::getenv("LPIC_ENC_WORKSPACE_MB");
+        const long long v = e ? atoll(e) : 4096;
+        return (int64_t)(v > 0 ? v : 4096) << 20;
+    }();
+    const int64_t per_img = N * ((int64_t)m->M * 4 + 3 * 4);
+    int chunk = n;
+    if ((int64_t)n * per_img > budget) chunk = (int)(budget / per_img > 1 ? budget / per_img : 1);
+    if (d_trace_raw || d_trace_cdf) chunk = n;                 // (traces index the whole batch)
+    if (int r = ensure(m->d_sw, m->sw_cap, (size_t)chunk * N * 3)) return r;
+    if (int r = ensure(m->d_raw, m->raw_cap, (size_t)chunk * N * m->M)) return r;
     CUDA_TRY(cudaMemsetAsync(d_status, 0, sizeof(int32_t) * n, st));
     const int64_t mc = (3 * N + RC_CH - 1) / RC_CH;
-    if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)n * mc)) return r;
-    if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)n * mc)) return r;
-    if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)n * (mc + 1))) return r;
-    if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)n * mc)) return r;
+    if (int r = ensure(m->d_rcR, m->rcR_cap, (size_t)chunk * mc)) return r;
+    if (int r = ensure(m->d_rcW, m->rcW_cap, (size_t)chunk * mc)) return r;
+    if (int r = ensure(m->d_rcP, m->rcP_cap, (size_t)chunk * (mc + 1))) return r;
+    if (int r = ensure(m->d_rcC, m->rcC_cap, (size_t)chunk * mc)) return r;
     const RcPlanWork pw{RcWork{m->d_rcR, m->d_rcW, m->d_rcP, m->d_rcC}, 3 * N};
-    int fused = 0;
-    if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images, n, H, W, mode, m->d_raw, m->d_sw, d_status,
-                                    d_trace_raw, d_trace_cdf, pw, &fused, st))
-        return r;
-    if (!fused && (rc_plan(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, st))) return LPIC_E_CUDA;
-    if (int r = rc_encode_finish(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, n, 3 * N, d_payload, cap_each, d_lens,
-                                 d_status, st))
-        return r;
-    m->launches = fused ? 4 : 5;
+    int launches = 0;
+    for (int b0 = 0; b0 < n; b0 += chunk) {
+        const int nb = n - b0 < chunk ? n - b0 : chunk;
+        int fused = 0;
+        if (int r = dispatch<EncodeRun>(m->CP, m->h, m, d_images + (size_t)b0 * N * 3, nb, H, W, mode, m->d_raw,
+                                        m->d_sw, d_status + b0, d_trace_raw, d_trace_cdf, pw, &fused, st))
+            return r;
+        if (!fused && (rc_plan(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, nb, 3 * N, st))) return LPIC_E_CUDA;
+        if (int r = rc_encode_finish(pw.wk, m->d_sw, nullptr, nullptr, 3 * N, nb, 3 * N,
+                                     d_payload + (size_t)b0 * cap_each, cap_each, d_lens + b0, d_status + b0, st))
+            return r;
+        launches += fused ? 4 : 5;
+    }
+    m->launches = launches;
     return 0;
 }
 
@@ -1398,6 +1438,7 @@ int lpic_decode_batch_device(lpic_model_t* m, const uint8_t* d_payload, const in
                              int n, int H, int W, int mode, uint8_t* d_images, int32_t* d_status, float* d_trace_raw,
                              int32_t* d_trace_cdf, void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     std::lock_guard<std::mutex> lk(m->mu);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1413,6 +1454,7 @@ int lpic_decode_batch_device(lpic_model_t* m, const uint8_t* d_payload, const in
 int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, int W, int mode, uint8_t* h_payload,
                       int64_t payload_cap, int64_t* h_offs, int64_t* h_lens, int32_t* h_status, void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = (int64_t)H * W;
@@ -1448,6 +1490,7 @@ int lpic_encode_batch(lpic_model_t* m, const uint8_t* h_images, int n, int H, in
 int lpic_decode_batch(lpic_model_t* m, const uint8_t* h_payload, const int64_t* h_offs, const int64_t* h_lens, int n,
                       int H, int W, int mode, uint8_t* h_images, int32_t* h_status, void* stream) {
     if (int r = check_geom(m, n, H, W, mode)) return r;
+    DeviceGuard dg_(m->device);
     if (n == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = (int64_t)H * W;

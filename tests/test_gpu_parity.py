@@ -573,3 +573,22 @@ def test_gpu_fast_filter_and_kernel_sizes_roundtrip(P, C, h):
         assert np.array_equal(a, b)
     got = sum(len(c.payload) for c in cs)
     assert abs(got - ref) <= 0.005 * ref + 8, (got, ref)
+
+
+@pytest.mark.gpu
+def test_gpu_devices_api_matches_single_device(P):
+    """encode_batch / decode_batch(devices=[...]): the batch is split into
+    contiguous slices, one host thread per device (shard.split_for_devices).
+    With one GPU the two slices share device 0, which still exercises the
+    threaded split, the per-thread device selection and the reassembly."""
+    import torch
+    from paper_2212_01185_b200 import synth
+    w, cfg = synth.baseline_weights()
+    imgs = [synth.synth_1f(40 + k, 24 + 4 * (k % 2), 20) for k in range(5)]     # two geometries
+    ref = P.encode_batch(imgs, w, cfg, "wave")
+    devs = [0] * max(2, torch.cuda.device_count())
+    got = P.encode_batch(imgs, w, cfg, "wave", devices=devs)
+    assert [c.to_bytes() for c in got] == [c.to_bytes() for c in ref]
+    out = P.decode_batch(got, w, cfg, devices=devs)
+    for a, b in zip(out, imgs):
+        assert np.array_equal(a, b)
