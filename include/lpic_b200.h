@@ -89,6 +89,21 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
 int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_cdf, int64_t N,
                           int32_t* d_syms, int32_t* d_status, void* stream);
 
+/* kernels._quantized_cdf (kernels.py:250-293) from explicit mixture
+ * parameters: d_pi, d_mu, d_s (N,K) f64 -> d_cdf (N,257) int32.  K <= 32. */
+int lpic_quantized_cdf(const double* d_pi, const double* d_mu, const double* d_s, int64_t N, int K, int dist,
+                       int32_t* d_cdf, void* stream);
+
+/* coder.RangeDecoder (coder.py:76-112), the interactive one-symbol-per-call
+ * API, as host code (a device round trip per symbol would cost ~500x the
+ * work; the codec's own decoding runs on the GPU).  h_data is copied.
+ * create/decode return 0, LPIC_S_CORRUPT (> 0) once the stream needed more
+ * than 3 virtual zero bytes (CorruptStreamError), or an LPIC_E_* code. */
+typedef struct lpic_rc_dec lpic_rc_dec_t;
+int lpic_rc_dec_create(const uint8_t* h_data, int64_t len, lpic_rc_dec_t** out);
+int lpic_rc_dec_decode(lpic_rc_dec_t* d, const int64_t* h_cdf /* 257 */, int32_t* h_sym);
+int lpic_rc_dec_destroy(lpic_rc_dec_t* d);
+
 /* kernels.true_symbol_probs (kernels.py:316-346): unquantised probability
  * of each coded symbol.  d_raw (N,M) f32, d_syms (N,3) int64, d_rn/d_gn (N)
  * f32 -> d_out (N,3) f64 */

@@ -33,7 +33,8 @@ EXPORTS = (
     "lpic_forward_full", "lpic_channel_cdfs", "lpic_rc_encode_streams", "lpic_rc_decode_tables",
     "lpic_encode_batch_device", "lpic_decode_batch_device", "lpic_encode_batch", "lpic_decode_batch",
     "lpic_last_launch_count", "lpic_true_symbol_probs", "lpic_theoretical_bits", "lpic_network_coding_order",
-    "lpic_mixture_loss_grad",
+    "lpic_mixture_loss_grad", "lpic_quantized_cdf", "lpic_rc_dec_create", "lpic_rc_dec_decode",
+    "lpic_rc_dec_destroy",
 )
 
 
@@ -81,6 +82,10 @@ def load(path: str = LIB_PATH):
     L.lpic_theoretical_bits.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_network_coding_order.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_mixture_loss_grad.argtypes = [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]
+    L.lpic_quantized_cdf.argtypes = [_vp, _vp, _vp, _i64, _i, _i, _vp, _vp]
+    L.lpic_rc_dec_create.argtypes = [_vp, _i64, C.POINTER(_vp)]
+    L.lpic_rc_dec_decode.argtypes = [_vp, _vp, _vp]
+    L.lpic_rc_dec_destroy.argtypes = [_vp]
     _lib = L
     return L
 

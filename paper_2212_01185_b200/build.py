@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "liblpic_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["lpic_kernels.cu", "lpic_decode_cp16.cu", "lpic_decode_cp32.cu", "lpic_decode_cp64.cu",
-           "lpic_decode_cp128.cu", "lpic_train.cu"]
+           "lpic_decode_cp128.cu", "lpic_train.cu", "lpic_host_rc.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 FLAGS = [

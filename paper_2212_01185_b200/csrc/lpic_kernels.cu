@@ -697,6 +697,32 @@ k_channel_cdfs(const float* __restrict__ raw, int64_t N, int M, int K, int dist,
     store_cdf_row(out + n * 257, start, mass);
 }
 
+// kernels._quantized_cdf (kernels.py:250-293) from explicit mixture
+// parameters: pi/mu/s (N, K) float64 -> cdf (N, 257) int32; one warp per
+// row, the same warp builder as the codec (z = (edge - mu) * (1/s)).
+__global__ void __launch_bounds__(128)
+k_quantized_cdf(const double* __restrict__ pi, const double* __restrict__ mu, const double* __restrict__ s, int64_t N,
+                int K, int dist, int32_t* __restrict__ out) {
+    __shared__ __align__(16) CdfConsts cc;
+    __shared__ WarpCdfScratch sc[4];
+    load_consts(&cc);
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n = (int64_t)blockIdx.x * 4 + wid;
+    if (n >= N) return;
+    double pi_l = 0.0, mu_l = 0.0, inv_l = 1.0;
+    if (lane < K) {
+        pi_l = pi[n * K + lane];
+        mu_l = mu[n * K + lane];
+        inv_l = __ddiv_rn(1.0, s[n * K + lane]);
+    }
+    double pmf[8];
+    warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, 0);
+    uint32_t start[8], mass[8];
+    warp_quantize(pmf, sc + wid, start, mass);
+    store_cdf_row(out + n * 257, start, mass);
+}
+
 __global__ void k_rc_decode_tables(const uint8_t* data, int64_t len, const int32_t* cdf, int64_t N,
                                    int32_t* syms, int32_t* status) {
     RcDecoder d;
@@ -1319,6 +1345,15 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
     const int r = rc_encode_parallel(ws, d_sw, d_off, d_cnt, 0, n_streams, mx, d_out, cap_each, d_len, d_status, st);
     CUDA_TRY(cudaStreamSynchronize(st));      // (the workspace is reused by the next call)
     return r;
+}
+
+int lpic_quantized_cdf(const double* d_pi, const double* d_mu, const double* d_s, int64_t N, int K, int dist,
+                       int32_t* d_cdf, void* stream) {
+    if (N < 0 || K < 1 || K > 32 || (dist != 0 && dist != 1)) return fail(LPIC_E_ARG, "bad argument");
+    if (N == 0) return 0;
+    k_quantized_cdf<<<(unsigned)((N + 3) / 4), 128, 0, (cudaStream_t)stream>>>(d_pi, d_mu, d_s, N, K, dist, d_cdf);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
 }
 
 int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_cdf, int64_t N, int32_t* d_syms,
