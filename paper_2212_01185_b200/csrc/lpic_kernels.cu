@@ -407,11 +407,11 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
             uint32_t start[8], mass[8];
             if constexpr (f32) {                            // FAST float32 tables (Gaussian)
                 float pmf[8];
-                warp_pmf32(__double2float_rn(pi_l), (float)mu_l, __double2float_rn(inv_l), K, &cc, pmf, ch * K);
+                warp_pmf32(__double2float_rn(pi_l), (float)mu_l, __double2float_rn(inv_l), K, &cc, pmf, ch * K, sc + wid);
                 warp_quantize32(pmf, sc + wid, start, mass);
             } else {
                 double pmf[8];
-                warp_pmf_t<dist>(pi_l, mu_l, inv_l, K, &cc, pmf, ch * K);
+                warp_pmf_t<dist>(pi_l, mu_l, inv_l, K, &cc, pmf, ch * K, sc + wid);
                 warp_quantize(pmf, sc + wid, start, mass);
             }
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);
@@ -717,7 +717,7 @@ k_quantized_cdf(const double* __restrict__ pi, const double* __restrict__ mu, co
         inv_l = __ddiv_rn(1.0, s[n * K + lane]);
     }
     double pmf[8];
-    warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, 0);
+    warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, 0, sc + wid);
     uint32_t start[8], mass[8];
     warp_quantize(pmf, sc + wid, start, mass);
     store_cdf_row(out + n * 257, start, mass);
@@ -1182,6 +1182,7 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
     m->net.ow = put(ow); m->net.ob = put(ob); m->net.mwI = put(mwI); m->net.hwI = put(hwI); m->net.owI = put(owI);
     m->net.C = C; m->net.CP = CP; m->net.M = M; m->net.MP = MP; m->net.NH = NH; m->net.T = T; m->net.TC = TC;
     m->net.MT = MT;
+    m->net.one = 1.0f;
     // fingerprint of the LPWT serialisation (network.py:255-281)
     std::vector<uint8_t> ser;
     const char magic[4] = {'L', 'P', 'W', 'T'};

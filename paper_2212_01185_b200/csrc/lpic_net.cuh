@@ -30,6 +30,7 @@ struct NetDev {                 // device-resident, padded weights
     const float* hwI;           // (NH, CP, CP) [l][in][out]
     const float* owI;           // (CP, MT)   [in][m], MT = M padded to 16
     int C, CP, M, MP, NH, T, TC, MT;
+    float one;                  // 1.0f at run time (tile_layer's packed FFMA2 must not fold it)
 };
 
 __device__ __forceinline__ float leaky(float x) { return x >= 0.0f ? x : __fmul_rn(0.01f, x); }
@@ -212,16 +213,40 @@ __device__ __forceinline__ void load_w(const float* p, float (&wv)[F]) {
     }
 }
 
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2): two pixels' products in one
+// instruction.  acc = fl(acc + fl(w * a)) stays two roundings: the product
+// is an FMUL2 and the sum an FFMA2 of that product times ONE, a runtime 1.0f
+// (NetDev::one) ptxas cannot fold -- with a literal 1.0 it contracts the
+// pair into a single fused FFMA2, which would change the result.  Both
+// IEEE-exact per lane (checked in scripts/ubench_phi_peak.cu on 2^23 pairs
+// and end to end by the bitwise network tests); the FP32 pipe rate is the
+// same, but half the issue slots leave room for the operand loads.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_mac(unsigned long long acc, unsigned long long w2, unsigned long long a2,
+                                                     unsigned long long one2) {
+    unsigned long long p, r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(w2), "l"(a2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(p), "l"(one2), "l"(acc));
+    return r;
+}
+
 // acc[p][f] = sum_{i<KD} W[i][og*F+f] * in[i][4pg+p], i ascending.  The
 // operands of row i+1 are loaded while row i is multiplied (register double
 // buffer), so the shared-memory latency hides behind the 8F products.
 template <int KD, int F>
 __device__ __forceinline__ void tile_layer(const float* in, const float* W, int nout, int og, int pg,
-                                           float (&acc)[4][F]) {
+                                           float (&acc)[4][F], float one) {
+    unsigned long long a01[F], a23[F];                  // pixel pairs (0,1), (2,3)
+    const unsigned long long one2 = f2_pack(one, one);
 #pragma unroll
-    for (int p = 0; p < 4; p++)
-#pragma unroll
-        for (int f = 0; f < F; f++) acc[p][f] = 0.0f;
+    for (int f = 0; f < F; f++) { a01[f] = 0ull; a23[f] = 0ull; }
     const float* ap = in + 4 * pg;
     const float* wp = W + og * F;
     float4 an = *reinterpret_cast<const float4*>(ap);
@@ -236,13 +261,18 @@ __device__ __forceinline__ void tile_layer(const float* in, const float* W, int 
         const int inext = i + 1 < KD ? i + 1 : i;       // the last row reloads itself (no branch)
         an = *reinterpret_cast<const float4*>(ap + inext * NT_TP);
         load_w<F>(wp + inext * nout, wn);
+        const unsigned long long x01 = f2_pack(a.x, a.y), x23 = f2_pack(a.z, a.w);
 #pragma unroll
         for (int f = 0; f < F; f++) {
-            acc[0][f] = __fadd_rn(acc[0][f], __fmul_rn(wv[f], a.x));
-            acc[1][f] = __fadd_rn(acc[1][f], __fmul_rn(wv[f], a.y));
-            acc[2][f] = __fadd_rn(acc[2][f], __fmul_rn(wv[f], a.z));
-            acc[3][f] = __fadd_rn(acc[3][f], __fmul_rn(wv[f], a.w));
+            const unsigned long long w2 = f2_pack(wv[f], wv[f]);
+            a01[f] = f2_mac(a01[f], w2, x01, one2);
+            a23[f] = f2_mac(a23[f], w2, x23, one2);
         }
+    }
+#pragma unroll
+    for (int f = 0; f < F; f++) {
+        f2_unpack(a01[f], acc[0][f], acc[1][f]);
+        f2_unpack(a23[f], acc[2][f], acc[3][f]);
     }
 }
 
@@ -250,7 +280,7 @@ __device__ __forceinline__ void tile_layer(const float* in, const float* W, int 
 template <int CP, int FO>
 __device__ __forceinline__ void tile_out(const NetDev& w, const float* in, const float* wo, int og, int pg, float* raw) {
     float acc[4][FO];
-    tile_layer<CP, FO>(in, wo, w.MT, og, pg, acc);
+    tile_layer<CP, FO>(in, wo, w.MT, og, pg, acc, w.one);
 #pragma unroll
     for (int f = 0; f < FO; f++) {
         const int m = og * FO + f;
@@ -290,7 +320,7 @@ __device__ void net_tile(const NetDev& w, NetTileBufs& b) {
     net_tile_wait(b, 0);
     if (t == 0) net_tile_load(w, b, 1, 1);
     if (worker) {
-        tile_layer<TC, F>(b.act0, b.wbuf, CP, og, pg, acc);
+        tile_layer<TC, F>(b.act0, b.wbuf, CP, og, pg, acc, w.one);
         tile_store_act<F>(acc, w.mb, og, pg, b.act1);
     }
     __syncthreads();
@@ -301,7 +331,7 @@ __device__ void net_tile(const NetDev& w, NetTileBufs& b) {
         net_tile_wait(b, buf);
         if (t == 0 && L + 1 < nl) net_tile_load(w, b, L + 1, buf ^ 1);
         if (worker) {
-            tile_layer<CP, F>(in, b.wbuf + (buf ? b.wstride : 0), CP, og, pg, acc);
+            tile_layer<CP, F>(in, b.wbuf + (buf ? b.wstride : 0), CP, og, pg, acc, w.one);
             tile_store_act<F>(acc, w.hb + l * CP, og, pg, out);
         }
         __syncthreads();
