@@ -63,7 +63,7 @@ CONFIGS = {
 # capture of the same workload (algorithmic: ~2 B per sub-pixel = image byte +
 # payload; the rest is the L2-resident record ring spilling to DRAM)
 NCU_TRAFFIC = {
-    ("c2", "compat", False): (64194560 + 28143872, "profiles/r1_sweep3/ncu_dec_c2_raw.csv"),
+    ("c2", "compat", False): (64089856 + 29096960, "profiles/r2/ncu_r2d/ncu_dec_c2_raw.csv"),
 }
 # measured on the box by scripts/ubench_phi_peak.cu / scripts/ubench_chain.cu
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r2", "ubench_peaks.json")

@@ -15,7 +15,7 @@ import paper_2212_01185_b200 as _impl
 from paper_2212_01185_b200 import *  # noqa: F401,F403
 
 _MODULES = ("codec", "coder", "errors", "kernels", "mixture", "network", "schedules", "synthetic", "training",
-            "tiles", "shard", "synth")
+            "images", "cli", "verification", "tiles", "shard", "synth")
 for _name in _MODULES:
     _mod = _importlib.import_module(f"paper_2212_01185_b200.{_name}")
     _sys.modules[f"{__name__}.{_name}"] = _mod

@@ -31,6 +31,7 @@
 #include "lpic_math.cuh"
 #include "lpic_net.cuh"
 #include "lpic_net_tc.cuh"
+#include "lpic_net_tc2.cuh"
 #include "lpic_rc.cuh"
 #include "lpic_sched.cuh"
 #include "lpic_decode_launch.h"
@@ -315,6 +316,135 @@ struct RcPlanArgs {
     int64_t* posc;
     int32_t* status;
 };
+
+// ---------------------------------------------------------------------------
+// encoder, stage 1 in FAST precision, pipelined (lpic_net_tc2.cuh): a
+// persistent CTA per SM owns pairs of 128-pixel tiles; warps 0-7 gather the
+// taps and run the epilogues of their tile, warp 8 issues the MMAs, warp 9
+// streams the weight blocks.  Bit-identical raw to k_enc_net_tc.
+// ---------------------------------------------------------------------------
+template <int HH>
+__global__ void __launch_bounds__(TC2_THREADS, 1)
+k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ images, int H, int W, int mode,
+              const int32_t* __restrict__ order, int64_t N, int n_img, float* __restrict__ raw_out, int32_t* status,
+              float* trace_raw) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    Tc2Smem* s = reinterpret_cast<Tc2Smem*>(smem);
+    __shared__ float lut[256];
+    constexpr int TC = Taps<HH>::TC;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int v = tid; v < 256; v += blockDim.x) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
+    if (warp == 8) umma::tmem_alloc(&s->tmem, 512);
+    if (tid == 0) {
+        for (int i = 0; i < 3; i++) { tc2_mbar_init(&s->wfull[i], 1); tc2_mbar_init(&s->wfree[i], 1); }
+        for (int t = 0; t < 2; t++) { tc2_mbar_init(&s->aready[t], 128); tc2_mbar_init(&s->dfull[t], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tbase = s->tmem;
+    const int64_t tiles_per = (N + TC_M - 1) / TC_M, total = tiles_per * n_img, pairs = (total + 1) / 2;
+    const int64_t my_pairs = (int64_t)blockIdx.x < pairs ? (pairs - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (warp == 9) {                                          // weight loader
+        if (lane == 0) {
+            const int64_t nblocks = my_pairs * w.nb;
+            for (int64_t g = 0; g < nblocks; g++) {
+                const int slot = (int)(g % 3), b = (int)(g % w.nb);
+                if (g >= 3) tc_mbar_wait(&s->wfree[slot], (uint32_t)(((g / 3) - 1) & 1));
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(umma::smem_addr(&s->wfull[slot])), "r"((uint32_t)w.blk_bytes[b]) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(umma::smem_addr(s->w[slot])), "l"(w.blk[b]), "r"((uint32_t)w.blk_bytes[b]),
+                             "r"(umma::smem_addr(&s->wfull[slot])) : "memory");
+            }
+        }
+    } else if (warp == 8) {                                   // MMA issue
+        if (lane == 0) {
+            uint32_t acnt[2] = {0u, 0u}, wcnt[3] = {0u, 0u, 0u};
+            int64_t g = 0;
+            for (int64_t p = 0; p < my_pairs; p++) {
+                for (int l = 0; l < w.nl; l++) {
+                    for (int t = 0; t < 2; t++) {
+                        tc_mbar_wait(&s->aready[t], acnt[t] & 1u);
+                        acnt[t]++;
+                        umma::fence_after();
+                        tc2_issue_layer(s, w, t, l, tbase, g, wcnt);
+                    }
+                    g += w.n_blk[l];
+                }
+            }
+        }
+    } else {                                                  // epilogue / gather: tile t, row r
+        const int t = warp >> 2, r = tid & 127;
+        const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+        const uint32_t dcol = tbase + (uint32_t)(256 * t);
+        unsigned char* a_hi = s->a_hi[t];
+        unsigned char* a_lo = s->a_lo[t];
+        uint32_t dcnt = 0;
+        for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+            const int64_t tile = 2 * p + t;
+            const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + r;
+            const bool valid = tile < total && n < N;
+            float x[TC];
+            if (valid) {
+                const int32_t ij = __ldg(order + n);
+                gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+            } else {
+#pragma unroll
+                for (int q = 0; q < TC; q++) x[q] = 0.0f;
+            }
+            tc2_store_input<TC>(a_hi, a_lo, r, x, w.K[0]);
+            umma::fence_async_smem();
+            umma::fence_before();
+            tc2_arrive(&s->aready[t]);
+            float* row = valid ? raw_out + (img * N + n) * w.M : nullptr;
+            bool finite = true;
+            for (int l = 0; l < w.nl; l++) {
+                tc_mbar_wait(&s->dfull[t], dcnt & 1u);
+                dcnt++;
+                umma::fence_after();
+                const bool last = l == w.nl - 1;
+                const int Nl = w.N[l], Knext = last ? 0 : w.K[l + 1];
+                for (int c0 = 0; c0 < Nl; c0 += 32) {
+                    float d0[32], d1[32];
+                    umma::tmem_ld32(dcol + lane_off + (uint32_t)c0, d0);
+                    umma::tmem_ld32(dcol + lane_off + (uint32_t)(TC_NMAX + c0), d1);
+                    float y[32];
+#pragma unroll
+                    for (int i = 0; i < 32; i++) {
+                        const float v = __fadd_rn(__fadd_rn(d0[i], __fmul_rn(d1[i], 4.8828125e-4f)),
+                                                  __ldg(w.bias[l] + c0 + i));
+                        y[i] = last ? v : (v >= 0.0f ? v : __fmul_rn(0.01f, v));
+                    }
+                    if (last) {
+                        if (row) {
+#pragma unroll
+                            for (int i = 0; i < 32; i++)
+                                if (c0 + i < w.M) {
+                                    row[c0 + i] = y[i];
+                                    finite &= isfinite(y[i]);
+                                    if (trace_raw) trace_raw[(img * N + n) * w.M + c0 + i] = y[i];
+                                }
+                        }
+                    } else if (c0 < Knext) {
+                        tc2_store_split(a_hi, a_lo, r, c0, Knext, y, (Knext - c0) >= 32 ? 4 : (Knext - c0) >> 3);
+                    }
+                }
+                umma::fence_before();
+                if (!last) {
+                    umma::fence_async_smem();
+                    tc2_arrive(&s->aready[t]);
+                }
+            }
+            if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (warp == 8) umma::tmem_dealloc(tbase, 512);
+}
 
 // ---------------------------------------------------------------------------
 // encoder, stage 2: three quantised CDF tables per pixel (warp builder) and
@@ -766,6 +896,9 @@ struct lpic_model {
     unsigned char* d_tc = nullptr;
     TcNetDev tcnet{};
     bool tc_ok = false;
+    unsigned char* d_tc2 = nullptr;        // K-blocked copy for k_enc_net_tc2
+    TcNet2Dev tcnet2{};
+    bool tc2_ok = false;
     // cached coding order per geometry
     int32_t* d_order = nullptr;
     int ord_H = -1, ord_W = -1, ord_mode = -1;
@@ -891,6 +1024,19 @@ int dispatch(int CP, int HH, A&&... args) {
 template <int HH>
 int launch_enc_net_tc(lpic_model* m, const uint8_t* d_images, int n, int H, int W, int mode, float* raw,
                       int32_t* d_status, float* tr, cudaStream_t st) {
+    static const bool v1 = std::getenv("LPIC_TC_V1") != nullptr;      // (A/B: the serial tile kernel)
+    if (m->tc2_ok && !v1) {
+        const size_t smem2 = sizeof(Tc2Smem);
+        if (set_smem(k_enc_net_tc2<HH>, smem2)) return LPIC_E_CUDA;
+        const int64_t N2 = (int64_t)H * W, tiles2 = ((N2 + TC_M - 1) / TC_M) * n, pairs = (tiles2 + 1) / 2;
+        int sms2 = 148;
+        cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, m->device);
+        const unsigned grid2 = (unsigned)(pairs < sms2 ? pairs : sms2);
+        k_enc_net_tc2<HH><<<grid2, TC2_THREADS, smem2, st>>>(m->tcnet2, d_images, H, W, mode, m->d_order, N2, n, raw,
+                                                             d_status, tr);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
     const size_t smem = sizeof(TcSmem);
     if (set_smem(k_enc_net_tc<HH>, smem)) return LPIC_E_CUDA;
     const int64_t N = (int64_t)H * W, tiles = ((N + TC_M - 1) / TC_M) * n;
@@ -1242,6 +1388,47 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
                 }
                 m->tc_ok = true;
             }
+            // the same weights as 64-column K blocks for the pipelined encoder
+            // network (k_enc_net_tc2): per block W_hi (N x Kb) | W_lo (N x Kb)
+            std::vector<int> bl, bk0, bkb;
+            for (int l = 0; l < nl; l++)
+                for (int k0 = 0; k0 < Ks[l]; k0 += TC2_KB) {
+                    bl.push_back(l); bk0.push_back(k0); bkb.push_back(Ks[l] - k0 < TC2_KB ? Ks[l] - k0 : TC2_KB);
+                }
+            if ((int)bl.size() <= TC2_MAXB && m->tc_ok) {
+                std::vector<size_t> boff2(bl.size());
+                size_t tot2 = 0;
+                for (size_t b = 0; b < bl.size(); b++) { boff2[b] = tot2; tot2 += (size_t)2 * Ns[bl[b]] * bkb[b] * 2; }
+                std::vector<unsigned char> hb2(tot2, 0);
+                for (size_t b = 0; b < bl.size(); b++) {
+                    const int l = bl[b], Nl = Ns[l], Kb = bkb[b], k0 = bk0[b];
+                    for (int n = 0; n < Nl; n++)
+                        for (int k = 0; k < Kb; k++) {
+                            // copy from the full-K canonical blob of layer l
+                            const size_t src = umma::op_offset(n, k0 + k, Ks[l]), dst = umma::op_offset(n, k, Kb);
+                            memcpy(&hb2[boff2[b] + dst], &hb[boff[l] + src], 2);
+                            memcpy(&hb2[boff2[b] + (size_t)Nl * Kb * 2 + dst], &hb[boff[l] + (size_t)Nl * Ks[l] * 2 + src], 2);
+                        }
+                }
+                if (cudaMalloc(&m->d_tc2, tot2) == cudaSuccess &&
+                    cudaMemcpy(m->d_tc2, hb2.data(), tot2, cudaMemcpyHostToDevice) == cudaSuccess) {
+                    TcNet2Dev& t2 = m->tcnet2;
+                    t2.nb = (int)bl.size(); t2.nl = nl; t2.M = M; t2.K0 = TC;
+                    for (int l = 0; l < nl; l++) {
+                        t2.N[l] = Ns[l]; t2.K[l] = Ks[l]; t2.bias[l] = m->tcnet.bias[l];
+                        t2.first_blk[l] = -1; t2.n_blk[l] = 0;
+                    }
+                    for (size_t b = 0; b < bl.size(); b++) {
+                        const int l = bl[b];
+                        t2.blk[b] = m->d_tc2 + boff2[b];
+                        t2.blk_bytes[b] = (int)(2 * Ns[l] * bkb[b] * 2);
+                        t2.blk_kb[b] = bkb[b]; t2.blk_k0[b] = bk0[b]; t2.blk_layer[b] = l;
+                        if (t2.first_blk[l] < 0) t2.first_blk[l] = (int)b;
+                        t2.n_blk[l]++;
+                    }
+                    m->tc2_ok = true;
+                }
+            }
         }
     }
     cudaError_t e = cudaGetLastError();
@@ -1260,6 +1447,7 @@ int lpic_model_destroy(lpic_model_t* m) {
     cudaFree(m->d_progress);
     cudaFree(m->d_rcR); cudaFree(m->d_rcW); cudaFree(m->d_rcP); cudaFree(m->d_rcC);
     cudaFree(m->d_tc);
+    cudaFree(m->d_tc2);
     cudaFree(m->d_ctr);
     delete m;
     return 0;

@@ -73,3 +73,27 @@ def test_status_and_precision_constants_match_header():
         if hasattr(_native, name):
             assert getattr(_native, name) == int(defs[name]), name
     assert int(defs["LPIC_PREC_COMPAT"]) == 0 and int(defs["LPIC_PREC_FAST"]) == 1
+
+
+@pytest.mark.parametrize("K,Cf,L,h,why", [
+    (17, 16, 4, 2, "mixtures"),       # the reference accepts any K >= 1 that fits a byte (network.py:49-59)
+    (3, 129, 4, 2, "filters"),
+    (3, 16, 4, 4, "kernel_half"),
+    (3, 16, 2, 2, "layers"),
+    (0, 16, 4, 2, "mixtures"),
+])
+def test_config_range_refused_loudly(K, Cf, L, h, why):
+    """The GPU build covers K <= 16, C <= 128, h <= 3, L >= 3 (every config
+    of the reference's tests and BASELINE); outside that range model
+    creation fails with a message before any device work -- never a silent
+    fallback.  Checked through the C-ABI without a GPU."""
+    from paper_2212_01185_b200 import _native
+    Lb = _native.load()
+    T = (2 * h + 1) * h + h
+    arrs = [np.zeros(n, np.float32) for n in (T * 3 * Cf, Cf, max(L - 2, 1) * Cf * Cf, max(L - 2, 1) * Cf,
+                                              12 * max(K, 1) * Cf, 12 * max(K, 1))]
+    out = C.c_void_p()
+    rc = Lb.lpic_model_create(*[a.ctypes.data for a in arrs], K, Cf, L, h, 0, C.byref(out))
+    assert rc in (_native.LPIC_E_UNSUPPORTED, _native.LPIC_E_ARG)
+    assert why.split("_")[0] in Lb.lpic_last_error().decode() or "layers" in Lb.lpic_last_error().decode()
+    assert not out.value

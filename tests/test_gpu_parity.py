@@ -592,3 +592,54 @@ def test_gpu_devices_api_matches_single_device(P):
     out = P.decode_batch(got, w, cfg, devices=devs)
     for a, b in zip(out, imgs):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_gpu_range_encoder_matches_reference_bytes():
+    """coder.RangeEncoder (symbols collected, coded on the GPU at finish())
+    reproduces the reference RangeEncoder's bytes (fixture written by
+    running the reference, oracle/gen_golden_dropin.py)."""
+    from paper_2212_01185_b200.coder import RangeDecoder, RangeEncoder
+    G = dict(np.load(os.path.join(GOLDEN, "reference_dropin.npz")))
+    enc = RangeEncoder()
+    for s, t in zip(G["rc_syms"], G["rc_picks"]):
+        enc.encode(int(s), G["rc_tables"][t])
+    pay = enc.finish()
+    assert pay == G["rc_payload"].tobytes()
+    with pytest.raises(RuntimeError):
+        enc.finish()
+    assert len(RangeEncoder().finish()) == 3                  # empty stream: the 3-byte flush
+    d = RangeDecoder(pay)
+    assert [d.decode(G["rc_tables"][t]) for t in G["rc_picks"][:50]] == [int(v) for v in G["rc_syms"][:50]]
+
+
+@pytest.mark.gpu
+def test_gpu_kernel_seam_quantized_cdf_and_invariants(P, oracle_mod):
+    """kernels._quantized_cdf on the GPU (explicit pi, mu, s) equals the C
+    oracle's red-channel table of a raw vector carrying those parameters
+    (pi, s formed with libm exp as in kernels._channel_mixture,
+    kernels.py:212-247), and the invariant suite (verification.run_all, the
+    reference's `verify`) passes against the GPU backend."""
+    import math
+    from paper_2212_01185_b200 import kernels, verification
+    rng = np.random.default_rng(77)
+    K = 3
+    for dist in (0, 1):
+        raws = rng.normal(0, 1.5, (40, 12 * K)).astype(np.float32)
+        raws[:, 6 * K:7 * K] = rng.uniform(-8, 3, (40, K)).astype(np.float32)
+        ref = oracle_mod.channel_cdfs(raws, K, dist, 0, np.zeros(40, np.float32), np.zeros(40, np.float32))
+        for n, raw in enumerate(raws):
+            lg = [float(v) for v in raw[:K]]
+            mx = max(lg)
+            e = [math.exp(v - mx) for v in lg]
+            tot = 0.0
+            for v in e:
+                tot += v
+            pi = np.array([v / tot for v in e])
+            mu = np.array([float(v) for v in raw[3 * K:4 * K]])
+            s = np.array([math.exp(min(max(float(v), -7.0), 7.0)) for v in raw[6 * K:7 * K]])
+            out = np.zeros(257, np.int64)
+            kernels._quantized_cdf(pi, mu, s, K, dist, kernels.EDGES, out)
+            assert np.array_equal(out, ref[n]), (dist, n)
+    results = verification.run_all(size=6)
+    assert all(r.passed for r in results), [(r.name, r.detail) for r in results if not r.passed]
