@@ -215,6 +215,8 @@ def run_reference(args, cfgd):
     w, cfg = synth.baseline_weights()
     if args.weights == "fitted":             # (the same fitted weights as our arm; fitting is not timed)
         w, cfg, _ = synth.fitted_weights()
+    elif args.weights == "flat":
+        w, cfg = synth.flat_weights()
     H, W = cfgd["H"], cfgd["W"]
     threads = os.cpu_count() or 1
     sub = dict(cfgd, n=min(cfgd["n"], threads), scaling="weak")
@@ -287,6 +289,8 @@ def run_ours(args, cfgd):
     fit_curve = None
     if args.weights == "fitted":
         w, cfg, fit_curve = synth.fitted_weights()
+    elif args.weights == "flat":
+        w, cfg = synth.flat_weights()
     H, W = cfgd["H"], cfgd["W"]
     N = H * W
     mode = P.parse_mode(args.mode)
@@ -436,7 +440,8 @@ def run_ours(args, cfgd):
             "config": {"workload": cfgd["desc"] + (" -- grayscale variant" if args.gray else ""),
                        "images_total": int(units_all / units_per_img), "images_rank0": n, "mode": args.mode,
                        "weights": ("kaiming seed 0 (K=3,C=128,L=5,h=2)" if args.weights == "kaiming" else
-                                   "kaiming seed 0 fitted 200 steps on the GPU trainer (K=3,C=128,L=5,h=2), "
+                                   "kaiming seed 0 with log-scale biases 7 (near-flat mixtures)" if args.weights == "flat"
+                                   else "kaiming seed 0 fitted 200 steps on the GPU trainer (K=3,C=128,L=5,h=2), "
                                    f"final train loss {fit_curve[-1].loss_bits_per_pixel / 3:.3f} bpsp"),
                        "precision": ("compat (bit-exact fp32 net)" if args.precision == "compat"
                                      else "fast (tcgen05 fp16x3 net)"),
@@ -529,8 +534,9 @@ def main():
     ap.add_argument("--parity-images", type=int, default=2,
                     help="byte-compare this many GPU containers with the C oracle (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--weights", default="kaiming", choices=["kaiming", "fitted"],
-                    help="BASELINE configs[1]: Kaiming seed 0, optionally fitted for 200 trainer steps")
+    ap.add_argument("--weights", default="kaiming", choices=["kaiming", "fitted", "flat"],
+                    help="BASELINE configs[1]: Kaiming seed 0, optionally fitted for 200 trainer steps; "
+                         "flat: log-scale biases at the e^7 clip (near-flat PMFs, the selection worst case)")
     ap.add_argument("--gray", action="store_true", help="grayscale variant (r=g=b replication, BASELINE configs[4])")
     ap.add_argument("--precision", default="compat", choices=["compat", "fast"],
                     help="compat: reference-exact fp32 network (default); fast: tcgen05 fp16x3 network")

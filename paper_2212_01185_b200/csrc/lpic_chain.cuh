@@ -50,6 +50,7 @@ struct ChainSmem {
     alignas(16) int wz[CH_WARPS];                 // per-warp count of digit-0 bins
     float wedgeq[CH_WARPS][KMAX];                 // (FAST) last upper edge as (Q, above-zero)
     int wedgep[CH_WARPS][KMAX];
+    alignas(16) uint32_t plus[8];                 // +1 bins of a crowded threshold bucket (bit k)
 };
 
 // key order of the reference's deficit selection: larger remainder first,
@@ -139,6 +140,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // E
     CHP(1);
     reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
+    if (t < 8) cs->plus[t] = 0u;
     float f0 = 0.0f, f1 = 0.0f;
 #pragma unroll
     for (int q = 0; q < KC; q++) {
@@ -211,6 +213,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // E
     CHP(1);
     reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
+    if (t < 8) cs->plus[t] = 0u;
     // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
     p0 = 0.0; p1 = 0.0;
 #pragma unroll
@@ -336,6 +339,26 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
             if (need == nB) {
                 bm |= mem;
+            } else if (nB > 24) {
+                // Crowded bucket (near-flat mixtures put most remainders in
+                // one digit): rank every member against all others with all
+                // 128 threads -- thread t its own bins 2t, 2t+1 -- instead of
+                // one member at a time (the loop below would take ~40k
+                // cycles).  Uniform across the chain's warps (B, nB, need come
+                // from the same shared data), so the two barriers are safe.
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const int k = 2 * t + u;
+                    if (cs->dig[k] == (uint8_t)B) {
+                        const double fk = cs->frac[k];
+                        int rank = 0;
+                        for (int j = 0; j < 256; j++)
+                            rank += (cs->dig[j] == (uint8_t)B) && beats(cs->frac[j], j, fk, k);
+                        if (rank < need) atomicOr(cs->plus + (k >> 5), 1u << (k & 31));
+                    }
+                }
+                chain_sync(bar);
+                bm |= (cs->plus[lane >> 2] >> (8 * (lane & 3))) & 0xFFu & mem;
             } else {
                 // exact ranks among the (few) members of B, frac desc / index asc
                 double fr[8];

@@ -334,10 +334,10 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
     constexpr int TC = Taps<HH>::TC;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int v = tid; v < 256; v += blockDim.x) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
-    if (warp == 8) umma::tmem_alloc(&s->tmem, 512);
+    if (warp == TC2_MMA_WARP) umma::tmem_alloc(&s->tmem, 512);
     if (tid == 0) {
         for (int i = 0; i < 3; i++) { tc2_mbar_init(&s->wfull[i], 1); tc2_mbar_init(&s->wfree[i], 1); }
-        for (int t = 0; t < 2; t++) { tc2_mbar_init(&s->aready[t], 128); tc2_mbar_init(&s->dfull[t], 1); }
+        for (int t = 0; t < 2; t++) { tc2_mbar_init(&s->aready[t], 256); tc2_mbar_init(&s->dfull[t], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     umma::fence_before();
@@ -346,7 +346,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
     const uint32_t tbase = s->tmem;
     const int64_t tiles_per = (N + TC_M - 1) / TC_M, total = tiles_per * n_img, pairs = (total + 1) / 2;
     const int64_t my_pairs = (int64_t)blockIdx.x < pairs ? (pairs - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    if (warp == 9) {                                          // weight loader
+    if (warp == TC2_LOAD_WARP) {                              // weight loader
         if (lane == 0) {
             const int64_t nblocks = my_pairs * w.nb;
             for (int64_t g = 0; g < nblocks; g++) {
@@ -359,7 +359,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                              "r"(umma::smem_addr(&s->wfull[slot])) : "memory");
             }
         }
-    } else if (warp == 8) {                                   // MMA issue
+    } else if (warp == TC2_MMA_WARP) {                        // MMA issue
         if (lane == 0) {
             uint32_t acnt[2] = {0u, 0u}, wcnt[3] = {0u, 0u, 0u};
             int64_t g = 0;
@@ -375,8 +375,11 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                 }
             }
         }
-    } else {                                                  // epilogue / gather: tile t, row r
-        const int t = warp >> 2, r = tid & 127;
+    } else {
+        // epilogue / gather: warps 0-15 -> tile t = (warp >> 2) & 1, row r
+        // (TMEM lane quadrant warp % 4), column half hf = warp >> 3: each
+        // thread handles 64 of a layer's (<= 128) output columns
+        const int t = (warp >> 2) & 1, hf = warp >> 3, r = 32 * (warp & 3) + lane;
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
         const uint32_t dcol = tbase + (uint32_t)(256 * t);
         unsigned char* a_hi = s->a_hi[t];
@@ -386,35 +389,43 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
             const int64_t tile = 2 * p + t;
             const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + r;
             const bool valid = tile < total && n < N;
-            float x[TC];
-            if (valid) {
-                const int32_t ij = __ldg(order + n);
-                gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
-            } else {
+            if (hf == 0) {                                    // the first layer's operand (all of K0)
+                float x[TC];
+                if (valid) {
+                    const int32_t ij = __ldg(order + n);
+                    gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+                } else {
 #pragma unroll
-                for (int q = 0; q < TC; q++) x[q] = 0.0f;
+                    for (int q = 0; q < TC; q++) x[q] = 0.0f;
+                }
+                tc2_store_input<TC>(a_hi, a_lo, r, x, w.K[0]);
+                umma::fence_async_smem();
             }
-            tc2_store_input<TC>(a_hi, a_lo, r, x, w.K[0]);
-            umma::fence_async_smem();
             umma::fence_before();
             tc2_arrive(&s->aready[t]);
             float* row = valid ? raw_out + (img * N + n) * w.M : nullptr;
             bool finite = true;
             for (int l = 0; l < w.nl; l++) {
+                const bool last = l == w.nl - 1;
+                const int Nl = w.N[l], Knext = last ? 0 : w.K[l + 1];
+                const float* bias = w.bias[l];
                 tc_mbar_wait(&s->dfull[t], dcnt & 1u);
                 dcnt++;
                 umma::fence_after();
-                const bool last = l == w.nl - 1;
-                const int Nl = w.N[l], Knext = last ? 0 : w.K[l + 1];
-                for (int c0 = 0; c0 < Nl; c0 += 32) {
+                for (int c0 = 64 * hf; c0 < Nl && c0 < 64 * hf + 64; c0 += 32) {
+                    float bv[32];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {             // (issued ahead of the TMEM loads)
+                        const float4 q4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
+                        bv[i] = q4.x; bv[i + 1] = q4.y; bv[i + 2] = q4.z; bv[i + 3] = q4.w;
+                    }
                     float d0[32], d1[32];
                     umma::tmem_ld32(dcol + lane_off + (uint32_t)c0, d0);
                     umma::tmem_ld32(dcol + lane_off + (uint32_t)(TC_NMAX + c0), d1);
                     float y[32];
 #pragma unroll
                     for (int i = 0; i < 32; i++) {
-                        const float v = __fadd_rn(__fadd_rn(d0[i], __fmul_rn(d1[i], 4.8828125e-4f)),
-                                                  __ldg(w.bias[l] + c0 + i));
+                        const float v = __fadd_rn(__fadd_rn(d0[i], __fmul_rn(d1[i], 4.8828125e-4f)), bv[i]);
                         y[i] = last ? v : (v >= 0.0f ? v : __fmul_rn(0.01f, v));
                     }
                     if (last) {
@@ -443,7 +454,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    if (warp == 8) umma::tmem_dealloc(tbase, 512);
+    if (warp == TC2_MMA_WARP) umma::tmem_dealloc(tbase, 512);
 }
 
 // ---------------------------------------------------------------------------

@@ -10,15 +10,16 @@
 // layer, one tile at a time (tensor pipe active ~9%, ncu r1).  Here a CTA
 // owns TWO tiles and four roles:
 //
-//   warps 0-3  epilogue of tile 0 (thread = row = TMEM lane)
-//   warps 4-7  epilogue of tile 1 (TMEM columns 256..511)
-//   warp 8     MMA issue: layer l of tile 0, then of tile 1, then l+1 ...
-//   warp 9     weight loader: 64-column K blocks (hi|lo, <= 32 KB) through a
-//              3-slot ring, each block used by both tiles then released
+//   warps 0-3, 8-11   epilogue of tile 0 (thread = row = TMEM lane; warps
+//                     0-3 output columns 0-63, 8-11 columns 64-127)
+//   warps 4-7, 12-15  epilogue of tile 1 (TMEM columns 256..511)
+//   warp 16           MMA issue: layer l of tile 0, then of tile 1, then l+1
+//   warp 17           weight loader: 64-column K blocks (hi|lo, <= 32 KB)
+//                     through a 3-slot ring, each used by both tiles
 //
 // so the epilogue of one tile (TMEM -> registers -> split -> smem) runs while
 // the tensor core works on the other tile's layer.  Hand-offs are mbarriers:
-// aready[t] (128 epilogue threads -> MMA: the tile's A operand for the next
+// aready[t] (256 epilogue threads -> MMA: the tile's A operand for the next
 // layer is in shared memory), dfull[t] (tcgen05.commit -> epilogue: the
 // layer's accumulators are in TMEM), wfull[s] (bulk copy landed), wfree[s]
 // (commit after tile 1's last MMA on the block).  Shared memory: 2 x 64 KB A
@@ -33,7 +34,8 @@ namespace lpic {
 constexpr int TC2_KB = 64;                                  // K columns per weight block
 constexpr int TC2_WBLK = 2 * TC_NMAX * TC2_KB * 2;          // bytes of one block (hi | lo), 32 KB
 constexpr int TC2_MAXB = 2 * TC_MAXL;                       // blocks per network pass
-constexpr int TC2_THREADS = 320;
+constexpr int TC2_MMA_WARP = 16, TC2_LOAD_WARP = 17;
+constexpr int TC2_THREADS = 32 * 18;           // 16 epilogue warps, MMA issue, weight loader
 
 struct TcNet2Dev {
     const unsigned char* blk[TC2_MAXB];   // per block: W_hi (N x Kb) | W_lo (N x Kb), canonical K-major, K = Kb

@@ -111,9 +111,11 @@ def channel_cdfs(raw, K, dist, channel, rn, gn, edges, out):
     if N == 0:
         return
     d_out = torch.empty((N, 257), dtype=torch.int32, device="cuda")
-    _native.check(L.lpic_channel_cdfs(_dev(raw, np.float32).data_ptr(), N, M, int(K), int(dist), int(channel),
-                                      _dev(rn, np.float32).data_ptr(), _dev(gn, np.float32).data_ptr(),
-                                      d_out.data_ptr(), _native.stream_ptr()), "lpic_channel_cdfs")
+    # (device copies held in locals: a temporary's memory could be recycled
+    # by the caching allocator before the kernel reads it)
+    d_raw, d_rn, d_gn = _dev(raw, np.float32), _dev(rn, np.float32), _dev(gn, np.float32)
+    _native.check(L.lpic_channel_cdfs(d_raw.data_ptr(), N, M, int(K), int(dist), int(channel), d_rn.data_ptr(),
+                                      d_gn.data_ptr(), d_out.data_ptr(), _native.stream_ptr()), "lpic_channel_cdfs")
     out[...] = d_out.cpu().numpy()
 
 
@@ -130,8 +132,7 @@ def _quantized_cdf(pi, mu, s, K, dist, edges, cdf, pmf=None, neg_rem=None):
     import torch
     L = _native.require_cuda()
     d_out = torch.empty((1, 257), dtype=torch.int32, device="cuda")
-    _native.check(L.lpic_quantized_cdf(_dev(np.asarray(pi)[:K], np.float64).data_ptr(),
-                                       _dev(np.asarray(mu)[:K], np.float64).data_ptr(),
-                                       _dev(np.asarray(s)[:K], np.float64).data_ptr(), 1, int(K), int(dist),
+    d_pi, d_mu, d_s = (_dev(np.asarray(a)[:K], np.float64) for a in (pi, mu, s))
+    _native.check(L.lpic_quantized_cdf(d_pi.data_ptr(), d_mu.data_ptr(), d_s.data_ptr(), 1, int(K), int(dist),
                                        d_out.data_ptr(), _native.stream_ptr()), "lpic_quantized_cdf")
     cdf[...] = d_out.cpu().numpy()[0]

@@ -86,3 +86,15 @@ def fitted_weights(steps: int = 200, seed: int = 0, n_train: int = 64, size: int
     tc = training.TrainConfig(batch_size=n_train, epochs=steps, seed=seed)   # one batch per epoch
     w, curve = training.train(imgs, tc, cfg, initial=w)
     return w, cfg, curve
+
+
+def flat_weights(log_scale: float = 7.0):
+    """Kaiming seed 0 with every mixture log-scale bias at `log_scale` (e^7:
+    the clip limit, network.py / kernels.py:242-247): near-flat PMFs whose
+    quantisation remainders mostly share one digit -- the worst case of the
+    deficit selection (the "flat-mixture cliff")."""
+    w, cfg = baseline_weights()
+    K = cfg.mixtures
+    w = w.copy()
+    w.out_b[6 * K:9 * K] = np.float32(log_scale)
+    return w, cfg

@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(NTH) k_check(int ncases, int K, int dist, floa
         const int ch = 1 + (c & 1);
         for (int m = threadIdx.x; m < 12 * K; m += blockDim.x) {
             uint32_t ss = s + 101 * m;
-            raw[m] = urand(ss, -scale, scale);
+            raw[m] = urand(ss, -fabsf(scale), fabsf(scale));
+            // scale < 0: near-flat mixtures (log-scales ~7: most remainders in one digit bucket)
+            if (scale < 0.0f && m >= 6 * K && m < 9 * K) raw[m] = urand(ss, 6.0f, 7.5f);
         }
         uint32_t s2 = s ^ 0xabcdefu;
         const float rn = urand(s2, -1.0f, 1.0f), gn = urand(s2, -1.0f, 1.0f);
@@ -161,11 +163,11 @@ int main() {
     int* bad; int32_t* rows; long long* d;
     cudaMalloc(&bad, 8); cudaMalloc(&rows, 4 * 600); cudaMalloc(&d, 64);
     const int Ks[4] = {3, 2, 5, 1};
-    const float scales[3] = {1.0f, 3.0f, 8.0f};
+    const float scales[4] = {1.0f, 3.0f, 8.0f, -1.0f};
     int total_bad = 0;
     for (int dist = 0; dist < 3; dist++)                 // 2: FAST float32 tables (Gaussian)
         for (int ki = 0; ki < 4; ki++)
-            for (int si = 0; si < 3; si++) {
+            for (int si = 0; si < 4; si++) {
                 cudaMemset(bad, 0, 8);
                 const int n = 4000;
                 if (dist == 2) k_check<true><<<296, NTH>>>(n, Ks[ki], 0, scales[si], bad, rows);
