@@ -90,9 +90,11 @@ int lpic_rc_decode_tables(const uint8_t* d_data, int64_t len, const int32_t* d_c
                           int32_t* d_syms, int32_t* d_status, void* stream);
 
 /* kernels._quantized_cdf (kernels.py:250-293) from explicit mixture
- * parameters: d_pi, d_mu, d_s (N,K) f64 -> d_cdf (N,257) int32.  K <= 32. */
+ * parameters: d_pi, d_mu, d_s (N,K) f64 -> d_cdf (N,257) int32.  K <= 32.
+ * Optional (NULL to skip): the kernel's scratch outputs as the reference
+ * leaves them, d_pmf (N,256) f64 and d_neg_rem (N,256) f64 = floor - value. */
 int lpic_quantized_cdf(const double* d_pi, const double* d_mu, const double* d_s, int64_t N, int K, int dist,
-                       int32_t* d_cdf, void* stream);
+                       int32_t* d_cdf, double* d_pmf, double* d_neg_rem, void* stream);
 
 /* coder.RangeDecoder (coder.py:76-112), the interactive one-symbol-per-call
  * API, as host code (a device round trip per symbol would cost ~500x the

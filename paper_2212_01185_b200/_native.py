@@ -82,7 +82,7 @@ def load(path: str = LIB_PATH):
     L.lpic_theoretical_bits.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_network_coding_order.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_mixture_loss_grad.argtypes = [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]
-    L.lpic_quantized_cdf.argtypes = [_vp, _vp, _vp, _i64, _i, _i, _vp, _vp]
+    L.lpic_quantized_cdf.argtypes = [_vp, _vp, _vp, _i64, _i, _i, _vp, _vp, _vp, _vp]
     L.lpic_rc_dec_create.argtypes = [_vp, _i64, C.POINTER(_vp)]
     L.lpic_rc_dec_decode.argtypes = [_vp, _vp, _vp]
     L.lpic_rc_dec_destroy.argtypes = [_vp]

@@ -342,21 +342,33 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             } else if (nB > 24) {
                 // Crowded bucket (near-flat mixtures put most remainders in
                 // one digit): rank every member against all others with all
-                // 128 threads -- thread t its own bins 2t, 2t+1 -- instead of
-                // one member at a time (the loop below would take ~40k
-                // cycles).  Uniform across the chain's warps (B, nB, need come
-                // from the same shared data), so the two barriers are safe.
+                // 128 threads -- thread t its own bins 2t, 2t+1, scanning the
+                // 256 (digit, remainder) pairs 8 at a time (broadcast shared
+                // loads) -- instead of one member at a time (~40k cycles).
+                // Uniform across the chain's warps (B, nB, need come from the
+                // same shared data), so the barrier below is safe.
+                const int ka = 2 * t;
+                const double fa = cs->frac[ka], fb = cs->frac[ka + 1];
+                const bool ma = cs->dig[ka] == (uint8_t)B, mb = cs->dig[ka + 1] == (uint8_t)B;
+                int ra = 0, rb = 0;
+                if (ma || mb) {
+#pragma unroll 2
+                    for (int j8 = 0; j8 < 256; j8 += 8) {
+                        const uint2 dv = *reinterpret_cast<const uint2*>(cs->dig + j8);
+                        const double2* f2 = reinterpret_cast<const double2*>(cs->frac + j8);
+                        const double2 q0 = f2[0], q1 = f2[1], q2 = f2[2], q3 = f2[3];
+                        const double fj[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
 #pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const int k = 2 * t + u;
-                    if (cs->dig[k] == (uint8_t)B) {
-                        const double fk = cs->frac[k];
-                        int rank = 0;
-                        for (int j = 0; j < 256; j++)
-                            rank += (cs->dig[j] == (uint8_t)B) && beats(cs->frac[j], j, fk, k);
-                        if (rank < need) atomicOr(cs->plus + (k >> 5), 1u << (k & 31));
+                        for (int u = 0; u < 8; u++) {
+                            const uint32_t d = ((u < 4 ? dv.x : dv.y) >> (8 * (u & 3))) & 0xFFu;
+                            const bool in = d == (uint32_t)B;
+                            ra += in && beats(fj[u], j8 + u, fa, ka);
+                            rb += in && beats(fj[u], j8 + u, fb, ka + 1);
+                        }
                     }
                 }
+                if (ma && ra < need) atomicOr(cs->plus + (ka >> 5), 1u << (ka & 31));
+                if (mb && rb < need) atomicOr(cs->plus + ((ka + 1) >> 5), 1u << ((ka + 1) & 31));
                 chain_sync(bar);
                 bm |= (cs->plus[lane >> 2] >> (8 * (lane & 3))) & 0xFFu & mem;
             } else {

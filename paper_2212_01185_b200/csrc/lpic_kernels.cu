@@ -359,20 +359,18 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                              "r"(umma::smem_addr(&s->wfull[slot])) : "memory");
             }
         }
-    } else if (warp == TC2_MMA_WARP) {                        // MMA issue
-        if (lane == 0) {
-            uint32_t acnt[2] = {0u, 0u}, wcnt[3] = {0u, 0u, 0u};
-            int64_t g = 0;
-            for (int64_t p = 0; p < my_pairs; p++) {
-                for (int l = 0; l < w.nl; l++) {
-                    for (int t = 0; t < 2; t++) {
-                        tc_mbar_wait(&s->aready[t], acnt[t] & 1u);
-                        acnt[t]++;
-                        umma::fence_after();
-                        tc2_issue_layer(s, w, t, l, tbase, g, wcnt);
-                    }
-                    g += w.n_blk[l];
+    } else if (warp == TC2_MMA_WARP) {                        // MMA issue (whole warp, elected lane)
+        uint32_t acnt[2] = {0u, 0u}, wcnt[3] = {0u, 0u, 0u};
+        int64_t g = 0;
+        for (int64_t p = 0; p < my_pairs; p++) {
+            for (int l = 0; l < w.nl; l++) {
+                for (int t = 0; t < 2; t++) {
+                    tc_mbar_wait(&s->aready[t], acnt[t] & 1u);
+                    acnt[t]++;
+                    umma::fence_after();
+                    tc2_issue_layer(s, w, t, l, tbase, g, wcnt);
                 }
+                g += w.n_blk[l];
             }
         }
     } else {
@@ -843,7 +841,7 @@ k_channel_cdfs(const float* __restrict__ raw, int64_t N, int M, int K, int dist,
 // row, the same warp builder as the codec (z = (edge - mu) * (1/s)).
 __global__ void __launch_bounds__(128)
 k_quantized_cdf(const double* __restrict__ pi, const double* __restrict__ mu, const double* __restrict__ s, int64_t N,
-                int K, int dist, int32_t* __restrict__ out) {
+                int K, int dist, int32_t* __restrict__ out, double* __restrict__ pmf_out, double* __restrict__ negrem_out) {
     __shared__ __align__(16) CdfConsts cc;
     __shared__ WarpCdfScratch sc[4];
     load_consts(&cc);
@@ -859,6 +857,20 @@ k_quantized_cdf(const double* __restrict__ pi, const double* __restrict__ mu, co
     }
     double pmf[8];
     warp_pmf(pi_l, mu_l, inv_l, K, dist, &cc, pmf, 0, sc + wid);
+    if (pmf_out || negrem_out) {                  // the reference kernel's scratch outputs (pmf, f - v)
+        unsigned long long qs = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) qs += fx_bin(pmf[q]);
+        const double scale = cdf_scale(fx_total(fx_warp_sum(qs)));
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const double v = __dmul_rn(pmf[q], scale);
+            double f = floor(v);
+            if (f > CDF_FLOOR) f = CDF_FLOOR;
+            if (pmf_out) pmf_out[n * 256 + 8 * lane + q] = pmf[q];
+            if (negrem_out) negrem_out[n * 256 + 8 * lane + q] = __dsub_rn(f, v);
+        }
+    }
     uint32_t start[8], mass[8];
     warp_quantize(pmf, sc + wid, start, mass);
     store_cdf_row(out + n * 257, start, mass);
@@ -1548,10 +1560,11 @@ int lpic_rc_encode_streams(const uint32_t* d_sw, const int64_t* d_off, const int
 }
 
 int lpic_quantized_cdf(const double* d_pi, const double* d_mu, const double* d_s, int64_t N, int K, int dist,
-                       int32_t* d_cdf, void* stream) {
+                       int32_t* d_cdf, double* d_pmf, double* d_neg_rem, void* stream) {
     if (N < 0 || K < 1 || K > 32 || (dist != 0 && dist != 1)) return fail(LPIC_E_ARG, "bad argument");
     if (N == 0) return 0;
-    k_quantized_cdf<<<(unsigned)((N + 3) / 4), 128, 0, (cudaStream_t)stream>>>(d_pi, d_mu, d_s, N, K, dist, d_cdf);
+    k_quantized_cdf<<<(unsigned)((N + 3) / 4), 128, 0, (cudaStream_t)stream>>>(d_pi, d_mu, d_s, N, K, dist, d_cdf,
+                                                                             d_pmf, d_neg_rem);
     CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -97,17 +97,27 @@ __device__ __forceinline__ void tc2_store_input(unsigned char* a_hi, unsigned ch
     }
 }
 
+__device__ __forceinline__ bool tc2_elect_one() {
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+    return p != 0;
+}
+
 // MMA issue for one (tile, layer): every K block of the layer, in order.
+// Executed by the whole MMA warp (so the descriptors stay warp-uniform, in
+// uniform registers); one elected lane issues each tcgen05 instruction.
 // gbase: global index (over the CTA's whole block stream) of the layer's
 // first block; the block's ring slot is its global index mod 3.  wcnt: uses
 // of each slot so far (tile 0 waits for the copy, tile 1 then releases it).
+// Descriptors are formed once per block: advancing a K=16 slice adds
+// (offset >> 4) to the 14-bit start-address field.
 __device__ __forceinline__ void tc2_issue_layer(Tc2Smem* s, const TcNet2Dev& w, int t, int l, uint32_t tbase,
                                                 int64_t gbase, uint32_t (&wcnt)[3]) {
     const int N = w.N[l], K = w.K[l];
     const uint32_t idesc = umma::idesc_f16(TC_M, N);
-    const uint32_t a_hi = umma::smem_addr(s->a_hi[t]), a_lo = umma::smem_addr(s->a_lo[t]);
     const uint32_t dcol = tbase + (uint32_t)(256 * t);
-    const uint32_t sbo_a = (uint32_t)(K * 16);
+    const uint64_t dah = umma::smem_desc(umma::smem_addr(s->a_hi[t]), 128, (uint32_t)(K * 16));
+    const uint64_t dal = umma::smem_desc(umma::smem_addr(s->a_lo[t]), 128, (uint32_t)(K * 16));
     for (int j = 0; j < w.n_blk[l]; j++) {
         const int b = w.first_blk[l] + j;
         const int slot = (int)((gbase + j) % 3);
@@ -117,21 +127,25 @@ __device__ __forceinline__ void tc2_issue_layer(Tc2Smem* s, const TcNet2Dev& w, 
             umma::fence_after();
         }
         const int Kb = w.blk_kb[b], k0 = w.blk_k0[b];
-        const uint32_t w_hi = umma::smem_addr(s->w[slot]), w_lo = w_hi + (uint32_t)(N * Kb * 2);
-        const uint32_t sbo_w = (uint32_t)(Kb * 16);
+        const uint32_t w_hi = umma::smem_addr(s->w[slot]);
+        const uint64_t dwh = umma::smem_desc(w_hi, 128, (uint32_t)(Kb * 16));
+        const uint64_t dwl = umma::smem_desc(w_hi + (uint32_t)(N * Kb * 2), 128, (uint32_t)(Kb * 16));
+        const uint64_t oa0 = (uint64_t)(k0 >> 3) * 8u;       // (k0 / 8) * 128 bytes, >> 4
         for (int kk = 0; kk < Kb; kk += 16) {
-            const int ks = (k0 + kk) >> 4;
-            const uint32_t oa = (uint32_t)((k0 + kk) >> 3) * 128u, ow = (uint32_t)(kk >> 3) * 128u;
-            umma::mma_f16(dcol, umma::smem_desc(a_hi + oa, 128, sbo_a), umma::smem_desc(w_hi + ow, 128, sbo_w), idesc,
-                          ks > 0);
-            umma::mma_f16(dcol + (uint32_t)TC_NMAX, umma::smem_desc(a_hi + oa, 128, sbo_a),
-                          umma::smem_desc(w_lo + ow, 128, sbo_w), idesc, ks > 0);
-            umma::mma_f16(dcol + (uint32_t)TC_NMAX, umma::smem_desc(a_lo + oa, 128, sbo_a),
-                          umma::smem_desc(w_hi + ow, 128, sbo_w), idesc, true);
+            const bool acc = (k0 + kk) > 0;
+            const uint64_t oa = oa0 + (uint64_t)(kk >> 3) * 8u, ow = (uint64_t)(kk >> 3) * 8u;
+            if (tc2_elect_one()) {
+                umma::mma_f16(dcol, dah + oa, dwh + ow, idesc, acc);
+                umma::mma_f16(dcol + (uint32_t)TC_NMAX, dah + oa, dwl + ow, idesc, acc);
+                umma::mma_f16(dcol + (uint32_t)TC_NMAX, dal + oa, dwh + ow, idesc, true);
+            }
+            __syncwarp();
         }
-        if (t == 1) umma::commit(&s->wfree[slot]);          // both tiles done with the block
+        if (t == 1 && tc2_elect_one()) umma::commit(&s->wfree[slot]);   // both tiles done with the block
+        __syncwarp();
     }
-    umma::commit(&s->dfull[t]);
+    if (tc2_elect_one()) umma::commit(&s->dfull[t]);
+    __syncwarp();
 }
 
 }  // namespace lpic

@@ -127,12 +127,20 @@ def true_symbol_probs(raw, syms, rn, gn, K, dist, edges, out):
 
 def _quantized_cdf(pi, mu, s, K, dist, edges, cdf, pmf=None, neg_rem=None):
     """One table from explicit mixture parameters (pi, mu, s: (K,) f64) ->
-    cdf (257,) int64.  pmf / neg_rem are the reference's scratch arrays and
-    are not written."""
+    cdf (257,) int64; like the reference kernel it also leaves the PMF in
+    `pmf` and floor - value in `neg_rem` (256 each) when they are given."""
     import torch
     L = _native.require_cuda()
     d_out = torch.empty((1, 257), dtype=torch.int32, device="cuda")
+    d_pmf = torch.empty((1, 256), dtype=torch.float64, device="cuda")
+    d_neg = torch.empty((1, 256), dtype=torch.float64, device="cuda")
     d_pi, d_mu, d_s = (_dev(np.asarray(a)[:K], np.float64) for a in (pi, mu, s))
     _native.check(L.lpic_quantized_cdf(d_pi.data_ptr(), d_mu.data_ptr(), d_s.data_ptr(), 1, int(K), int(dist),
-                                       d_out.data_ptr(), _native.stream_ptr()), "lpic_quantized_cdf")
+                                       d_out.data_ptr(), d_pmf.data_ptr() if pmf is not None else None,
+                                       d_neg.data_ptr() if neg_rem is not None else None, _native.stream_ptr()),
+                  "lpic_quantized_cdf")
     cdf[...] = d_out.cpu().numpy()[0]
+    if pmf is not None:
+        pmf[...] = d_pmf.cpu().numpy()[0]
+    if neg_rem is not None:
+        neg_rem[...] = d_neg.cpu().numpy()[0]
