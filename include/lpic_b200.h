@@ -154,6 +154,10 @@ int lpic_last_launch_count(const lpic_model_t* m);
  * and, if d_draw is not null, d loss / d raw (N, 12K) f32. */
 int lpic_mixture_loss_grad(const float* d_raw, const uint8_t* d_images, int64_t N, int K, int dist, double* d_logp,
                            float* d_draw, void* stream);
+/* The same on float64 network outputs (the reference's float64 training
+ * path, training.py:219-240, used by finite_difference_check). */
+int lpic_mixture_loss_grad_f64(const double* d_raw, const uint8_t* d_images, int64_t N, int K, int dist,
+                               double* d_logp, double* d_draw, void* stream);
 
 #ifdef __cplusplus
 }

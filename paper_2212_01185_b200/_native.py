@@ -34,7 +34,7 @@ EXPORTS = (
     "lpic_encode_batch_device", "lpic_decode_batch_device", "lpic_encode_batch", "lpic_decode_batch",
     "lpic_last_launch_count", "lpic_true_symbol_probs", "lpic_theoretical_bits", "lpic_network_coding_order",
     "lpic_mixture_loss_grad", "lpic_quantized_cdf", "lpic_rc_dec_create", "lpic_rc_dec_decode",
-    "lpic_rc_dec_destroy",
+    "lpic_rc_dec_destroy", "lpic_mixture_loss_grad_f64",
 )
 
 
@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH):
     L.lpic_theoretical_bits.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_network_coding_order.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp, _vp]
     L.lpic_mixture_loss_grad.argtypes = [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]
+    L.lpic_mixture_loss_grad_f64.argtypes = [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]
     L.lpic_quantized_cdf.argtypes = [_vp, _vp, _vp, _i64, _i, _i, _vp, _vp, _vp, _vp]
     L.lpic_rc_dec_create.argtypes = [_vp, _i64, C.POINTER(_vp)]
     L.lpic_rc_dec_decode.argtypes = [_vp, _vp, _vp]

@@ -264,8 +264,11 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         // tails, where most bins would collide -- counted per warp instead)
         const int d0 = min(__double2int_rz(__dmul_rn(fr0, 256.0)), 255);
         const int d1 = min(__double2int_rz(__dmul_rn(fr1, 256.0)), 255);
-        if (d0) atomicAdd(cs->hist + d0, 1u);
-        if (d1) atomicAdd(cs->hist + d1, 1u);
+        // lanes with equal digits add once (near-flat mixtures: a whole warp
+        // shares one digit, and 64 same-address atomics would serialise)
+        const uint32_t k0 = __match_any_sync(0xffffffffu, d0), k1 = __match_any_sync(0xffffffffu, d1);
+        if (d0 && lane == __ffs(k0) - 1) atomicAdd(cs->hist + d0, (uint32_t)__popc(k0));
+        if (d1 && lane == __ffs(k1) - 1) atomicAdd(cs->hist + d1, (uint32_t)__popc(k1));
         const int zc = __reduce_add_sync(0xffffffffu, (d0 == 0) + (d1 == 0));
         if (lane == 0) cs->wz[w] = zc;
         reinterpret_cast<double2*>(cs->frac)[t] = make_double2(fr0, fr1);

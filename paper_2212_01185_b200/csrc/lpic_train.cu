@@ -40,13 +40,16 @@ __device__ __forceinline__ void cdf_pdf(double z, int dist, double& F, double& f
     }
 }
 
+// R: float32 network outputs (the trainer) or float64 (the reference's
+// float64 path: finite-difference checks)
+template <typename R>
 __global__ void __launch_bounds__(128)
-k_mixture_loss(const float* __restrict__ raw, const uint8_t* __restrict__ images, int64_t N, int K, int dist,
-               double* __restrict__ logp_out, float* __restrict__ draw) {
+k_mixture_loss(const R* __restrict__ raw, const uint8_t* __restrict__ images, int64_t N, int K, int dist,
+               double* __restrict__ logp_out, R* __restrict__ draw) {
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     const int M = 12 * K;
-    const float* r = raw + n * M;
+    const R* r = raw + n * M;
     const int sym[3] = {images[3 * n], images[3 * n + 1], images[3 * n + 2]};
     const double rn = (2.0 * sym[0] - 255.0) / 255.0, gn = (2.0 * sym[1] - 255.0) / 255.0;
     const double scale = 1.0 / ((double)N * TR_LN2);
@@ -90,28 +93,28 @@ k_mixture_loss(const float* __restrict__ raw, const uint8_t* __restrict__ images
         const double logp = jmax + log(jsum);
         total += logp;
         if (draw) {
-            float* d = draw + n * M;
+            R* d = draw + n * M;
             for (int k = 0; k < K; k++) {
                 const double pi = exp((double)r[ch * K + k] - lmax - llog);
                 const double q = exp(joint[k] - logp);
-                d[ch * K + k] = (float)((pi - q) * scale);                                  // dlogits
+                d[ch * K + k] = (R)((pi - q) * scale);                                  // dlogits
                 const double A = P[k] > TR_FLOOR ? q / fmax(P[k], TR_FLOOR) * scale : 0.0;
                 const double dm = A * (fu_[k] - fl_[k]) / sd[k];
                 dmu_eff[ch][k] = dm;
-                d[3 * K + ch * K + k] = (float)dm;                                          // dmu
+                d[3 * K + ch * K + k] = (R)dm;                                          // dmu
                 const double zfl = isfinite(zl_[k]) ? zl_[k] * fl_[k] : 0.0;
                 const double zfu = isfinite(zu_[k]) ? zu_[k] * fu_[k] : 0.0;
-                d[6 * K + ch * K + k] = (float)(open_s[k] ? A * (zfu - zfl) : 0.0);         // drho
+                d[6 * K + ch * K + k] = (R)(open_s[k] ? A * (zfu - zfl) : 0.0);         // drho
             }
         }
     }
     logp_out[n] = total;
     if (draw) {
-        float* d = draw + n * M;
+        R* d = draw + n * M;
         for (int k = 0; k < K; k++) {                       // dcoef through tanh (training.py:199-203)
-            d[9 * K + 0 * K + k] = (float)(dmu_eff[1][k] * rn * (1.0 - tanhv[0][k] * tanhv[0][k]));
-            d[9 * K + 1 * K + k] = (float)(dmu_eff[2][k] * rn * (1.0 - tanhv[1][k] * tanhv[1][k]));
-            d[9 * K + 2 * K + k] = (float)(dmu_eff[2][k] * gn * (1.0 - tanhv[2][k] * tanhv[2][k]));
+            d[9 * K + 0 * K + k] = (R)(dmu_eff[1][k] * rn * (1.0 - tanhv[0][k] * tanhv[0][k]));
+            d[9 * K + 1 * K + k] = (R)(dmu_eff[2][k] * rn * (1.0 - tanhv[1][k] * tanhv[1][k]));
+            d[9 * K + 2 * K + k] = (R)(dmu_eff[2][k] * gn * (1.0 - tanhv[2][k] * tanhv[2][k]));
         }
     }
 }
@@ -123,7 +126,17 @@ extern "C" int lpic_mixture_loss_grad(const float* d_raw, const uint8_t* d_image
     if (N < 0 || K < 1 || K > TR_KMAX || (dist != 0 && dist != 1) || !d_raw || !d_images || !d_logp)
         return LPIC_E_ARG;
     if (N == 0) return 0;
-    k_mixture_loss<<<(unsigned)((N + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_raw, d_images, N, K, dist, d_logp,
-                                                                                  d_draw);
+    k_mixture_loss<float><<<(unsigned)((N + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_raw, d_images, N, K, dist,
+                                                                                         d_logp, d_draw);
+    return cudaGetLastError() == cudaSuccess ? 0 : LPIC_E_CUDA;
+}
+
+extern "C" int lpic_mixture_loss_grad_f64(const double* d_raw, const uint8_t* d_images, int64_t N, int K, int dist,
+                                          double* d_logp, double* d_draw, void* stream) {
+    if (N < 0 || K < 1 || K > TR_KMAX || (dist != 0 && dist != 1) || !d_raw || !d_images || !d_logp)
+        return LPIC_E_ARG;
+    if (N == 0) return 0;
+    k_mixture_loss<double><<<(unsigned)((N + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_raw, d_images, N, K,
+                                                                                          dist, d_logp, d_draw);
     return cudaGetLastError() == cudaSuccess ? 0 : LPIC_E_CUDA;
 }

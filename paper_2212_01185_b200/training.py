@@ -84,9 +84,21 @@ def _fp32_gemms():
         torch.backends.cuda.matmul.allow_tf32 = old
 
 
-def _device_weights(w: Weights):
+def _float_type(dtype):
+    """numpy float32 / float64 -> the matching torch dtype (the reference's
+    float64 path is the finite-difference oracle)."""
     import torch
-    return [torch.from_numpy(np.ascontiguousarray(t, np.float32)).cuda() for t in w.tensors()]
+    d = np.dtype(dtype)
+    if d == np.float32:
+        return torch.float32
+    if d == np.float64:
+        return torch.float64
+    raise ValueError("the trainer runs in float32 or float64")
+
+
+def _device_weights(w: Weights, dtype=np.float32):
+    import torch
+    return [torch.from_numpy(np.ascontiguousarray(t, dtype)).cuda() for t in w.tensors()]
 
 
 def _gather_causal(x, taps):
@@ -148,37 +160,42 @@ def _check_batch(batch):
         raise ValueError("expected a nonempty (B, H, W, 3) uint8 batch")
 
 
-def _loss_grad_device(d_batch, dw, cfg: ModelConfig, want_grad: bool):
-    """Device batch (B, H, W, 3) u8 -> (loss, [6 gradient tensors] | None)."""
+def _mixture_device(raw, d_pix, cfg: ModelConfig, want_grad: bool):
+    """raw (N, 12K) float32/float64 device tensor, d_pix (N, 3) u8 -> (mean
+    -log2 p per pixel, d loss / d raw | None), the fused likelihood kernel
+    (training._mixture_loss, training.py:138-213)."""
     import torch
     L = _native.require_cuda()
-    B, H, W, _ = d_batch.shape
-    N = B * H * W
-    x = d_batch.to(torch.float32) / 127.5 - 1.0                 # training._normalize_batch (float32)
+    N = raw.shape[0]
+    raw = raw.contiguous()
+    logp = torch.empty(N, dtype=torch.float64, device=raw.device)
+    draw = torch.empty_like(raw) if want_grad else None
+    fn = L.lpic_mixture_loss_grad_f64 if raw.dtype == torch.float64 else L.lpic_mixture_loss_grad
+    _native.check(fn(raw.data_ptr(), d_pix.data_ptr(), N, cfg.mixtures, int(cfg.distribution), logp.data_ptr(),
+                     draw.data_ptr() if want_grad else None, _native.stream_ptr()), "mixture loss")
+    return float(-logp.sum().item() / N / LN2), draw
+
+
+def _loss_grad_device(d_batch, dw, cfg: ModelConfig, want_grad: bool, dtype=np.float32):
+    """Device batch (B, H, W, 3) u8 -> (loss, [6 gradient tensors] | None)."""
+    tdt = _float_type(dtype)
+    x = d_batch.to(tdt) / 127.5 - 1.0                         # training._normalize_batch
     taps = causal_taps(cfg.kernel_half)
     with _fp32_gemms():
         x1 = _gather_causal(x, taps)
         raw, zs = _forward(x1, dw, cfg)
-        raw = raw.contiguous()
-        logp = torch.empty(N, dtype=torch.float64, device=raw.device)
-        draw = torch.empty_like(raw) if want_grad else None
-        _native.check(L.lpic_mixture_loss_grad(raw.data_ptr(), d_batch.data_ptr(), N, cfg.mixtures,
-                                               int(cfg.distribution), logp.data_ptr(),
-                                               draw.data_ptr() if want_grad else None, _native.stream_ptr()),
-                      "mixture loss")
-        value = float(-logp.sum().item() / N / LN2)
+        value, draw = _mixture_device(raw, d_batch.reshape(-1, 3), cfg, want_grad)
         grads = _backward(draw, x1, zs, dw, cfg) if want_grad else None
     return value, grads
 
 
 def loss(batch: np.ndarray, w: Weights, cfg: ModelConfig, dtype=np.float32) -> float:
     """Mean -log2 P(r, g, b | context) per pixel over the batch, in bits
-    (training.py:219-228)."""
+    (training.py:219-228); dtype float32 (the trainer) or float64."""
     import torch
     _check_batch(batch)
-    if np.dtype(dtype) != np.float32:
-        raise ValueError("the GPU trainer runs the network in float32")
-    value, _ = _loss_grad_device(torch.from_numpy(np.ascontiguousarray(batch)).cuda(), _device_weights(w), cfg, False)
+    value, _ = _loss_grad_device(torch.from_numpy(np.ascontiguousarray(batch)).cuda(), _device_weights(w, dtype),
+                                 cfg, False, dtype)
     return value
 
 
@@ -186,10 +203,94 @@ def backward(batch: np.ndarray, w: Weights, cfg: ModelConfig, dtype=np.float32) 
     """Loss plus analytic gradients for every weight tensor (training.py:231-240)."""
     import torch
     _check_batch(batch)
-    if np.dtype(dtype) != np.float32:
-        raise ValueError("the GPU trainer runs the network in float32")
-    value, g = _loss_grad_device(torch.from_numpy(np.ascontiguousarray(batch)).cuda(), _device_weights(w), cfg, True)
+    value, g = _loss_grad_device(torch.from_numpy(np.ascontiguousarray(batch)).cuda(), _device_weights(w, dtype),
+                                 cfg, True, dtype)
     return value, GradientSet(*[t.cpu().numpy() for t in g])
+
+
+# The reference's internal stages, with the same arguments (its tests call
+# them): host arrays in and out, the work on the GPU.
+def _normalize_batch(images: np.ndarray, dtype):
+    x = images.astype(dtype)
+    return x / dtype(127.5) - dtype(1.0)
+
+
+def _network_forward(xn: np.ndarray, w: Weights, cfg: ModelConfig, dtype):
+    """(B, H, W, 3) normalised -> raw (B, H, W, M) and the backward cache
+    (gathered taps, pre-activations; device tensors)."""
+    import torch
+    B, H, W, _ = xn.shape
+    dw = _device_weights(w, dtype)
+    with _fp32_gemms():
+        x1 = _gather_causal(torch.from_numpy(np.ascontiguousarray(xn, dtype)).cuda(), causal_taps(cfg.kernel_half))
+        raw, zs = _forward(x1, dw, cfg)
+    return raw.reshape(B, H, W, cfg.param_channels).cpu().numpy(), (x1, zs)
+
+
+def _network_backward(draw, cache, w: Weights, cfg: ModelConfig) -> GradientSet:
+    import torch
+    x1, zs = cache
+    dw = _device_weights(w, np.float64 if x1.dtype == torch.float64 else np.float32)
+    d = torch.from_numpy(np.ascontiguousarray(draw).reshape(x1.shape[0], cfg.param_channels)).to(x1)
+    with _fp32_gemms():
+        g = _backward(d, x1, zs, dw, cfg)
+    return GradientSet(*[t.cpu().numpy() for t in g])
+
+
+def _mixture_loss(raw, images, cfg: ModelConfig, want_grad: bool):
+    """(loss in bits per pixel, d loss / d raw shaped like raw | None)."""
+    import torch
+    r = np.ascontiguousarray(raw)
+    value, draw = _mixture_device(torch.from_numpy(r.reshape(-1, cfg.param_channels)).cuda(),
+                                  torch.from_numpy(np.ascontiguousarray(images, np.uint8).reshape(-1, 3)).cuda(),
+                                  cfg, want_grad)
+    return value, (draw.cpu().numpy().reshape(r.shape) if want_grad else None)
+
+
+def finite_difference_check(cfg: ModelConfig | None = None, checks: int = 200, seed: int = 0, eps: float = 1e-3,
+                            batch_shape=(2, 8, 8)):
+    """Analytic (GPU backward, float64) vs central finite-difference
+    gradients at randomly drawn scalar parameters; the reference's check
+    (training.py:352-414): randomised biases, draws whose +-eps window
+    crosses a LeakyReLU kink are redrawn.  Returns (worst relative error,
+    [(tensor, index, analytic, numeric, rel)])."""
+    cfg = cfg or ModelConfig(mixtures=2, filters=8, layers=4)
+    rng = np.random.default_rng(seed)
+    B, H, W = batch_shape
+    batch = rng.integers(0, 256, (B, H, W, 3), dtype=np.uint8)
+    w32 = glorot_weights(cfg, rng)
+    for b in (w32.masked_b, w32.hidden_b, w32.out_b):
+        b[:] = rng.uniform(-0.3, 0.3, b.shape)
+    w = Weights(*[t.astype(np.float64) for t in w32.tensors()])
+    _, grads = backward(batch, w, cfg, dtype=np.float64)
+    xn = _normalize_batch(batch, np.float64)
+
+    def at_current():
+        raw, (_, zs) = _network_forward(xn, w, cfg, np.float64)
+        return _mixture_loss(raw, batch, cfg, want_grad=False)[0], zs
+
+    params, gparams = w.tensors(), grads.tensors()
+    records, worst, tries = [], 0.0, 0
+    while len(records) < checks:
+        tries += 1
+        if tries > 50 * checks:
+            raise LpicError("gradient check could not find enough kink-free draws")
+        ti = int(rng.integers(0, len(params)))
+        k = int(rng.integers(0, params[ti].size))
+        x0 = float(params[ti].flat[k])
+        params[ti].flat[k] = x0 + eps
+        up, z_up = at_current()
+        params[ti].flat[k] = x0 - eps
+        down, z_dn = at_current()
+        params[ti].flat[k] = x0
+        if any(bool(((a >= 0) != (b >= 0)).any()) for a, b in zip(z_up, z_dn)):
+            continue
+        numeric = (up - down) / (2.0 * eps)
+        analytic = float(gparams[ti].flat[k])
+        rel = abs(numeric - analytic) / max(abs(numeric), abs(analytic), 1e-6)
+        worst = max(worst, rel)
+        records.append((ti, k, analytic, numeric, rel))
+    return worst, records
 
 
 class Adam:

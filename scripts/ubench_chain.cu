@@ -227,6 +227,13 @@ int main() {
     const char* nm[14] = {"P cdf", "bar E", "pmf+fx", "bar T", "Q rest", "bar A", "S level2+", "prefix", "-", "D search",
                           "Q scale", "P z", "P phi", "S level1"};
     for (int i = 0; i < 14; i++) printf("  %-10s %6lld cycles/table\n", nm[i], hp[i] / 4000);
+    {   // the same phases on near-flat mixtures (crowded threshold bucket)
+        k_time<false><<<1, NTH>>>(2000, d, 0.001);
+        long long hf[2]; cudaMemcpy(hf, d, 16, cudaMemcpyDeviceToHost);
+        printf("chain_table K=3 flat: %lld cycles per table\n", hf[0]);
+        cudaMemcpyFromSymbol(hp, g_prof, sizeof(hp));
+        for (int i = 0; i < 14; i++) printf("  flat %-10s %6lld cycles/table\n", nm[i], hp[i] / 2000);
+    }
 #endif
     printf("TOTAL mismatches %d\n", total_bad);
     return total_bad != 0;
