@@ -50,7 +50,7 @@ struct ChainSmem {
     alignas(16) int wz[CH_WARPS];                 // per-warp count of digit-0 bins
     float wedgeq[CH_WARPS][KMAX];                 // (FAST) last upper edge as (Q, above-zero)
     int wedgep[CH_WARPS][KMAX];
-    alignas(16) uint32_t plus[8];                 // +1 bins of a crowded threshold bucket (bit k)
+    alignas(16) uint32_t whist[CH_WARPS][256];    // per-warp histograms of a crowded threshold bucket
 };
 
 // key order of the reference's deficit selection: larger remainder first,
@@ -140,7 +140,6 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // E
     CHP(1);
     reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
-    if (t < 8) cs->plus[t] = 0u;
     float f0 = 0.0f, f1 = 0.0f;
 #pragma unroll
     for (int q = 0; q < KC; q++) {
@@ -213,7 +212,6 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     chain_sync(bar);                                                                        // E
     CHP(1);
     reinterpret_cast<uint2*>(cs->hist)[t] = make_uint2(0u, 0u);    // (read by every warp until its E)
-    if (t < 8) cs->plus[t] = 0u;
     // PMF (kernels.py:264-271): pmf[k] += pi_i * d for d > 0, components in order
     p0 = 0.0; p1 = 0.0;
 #pragma unroll
@@ -264,11 +262,8 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         // tails, where most bins would collide -- counted per warp instead)
         const int d0 = min(__double2int_rz(__dmul_rn(fr0, 256.0)), 255);
         const int d1 = min(__double2int_rz(__dmul_rn(fr1, 256.0)), 255);
-        // lanes with equal digits add once (near-flat mixtures: a whole warp
-        // shares one digit, and 64 same-address atomics would serialise)
-        const uint32_t k0 = __match_any_sync(0xffffffffu, d0), k1 = __match_any_sync(0xffffffffu, d1);
-        if (d0 && lane == __ffs(k0) - 1) atomicAdd(cs->hist + d0, (uint32_t)__popc(k0));
-        if (d1 && lane == __ffs(k1) - 1) atomicAdd(cs->hist + d1, (uint32_t)__popc(k1));
+        if (d0) atomicAdd(cs->hist + d0, 1u);
+        if (d1) atomicAdd(cs->hist + d1, 1u);
         const int zc = __reduce_add_sync(0xffffffffu, (d0 == 0) + (d1 == 0));
         if (lane == 0) cs->wz[w] = zc;
         reinterpret_cast<double2*>(cs->frac)[t] = make_double2(fr0, fr1);
@@ -344,36 +339,15 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
                 bm |= mem;
             } else if (nB > 24) {
                 // Crowded bucket (near-flat mixtures put most remainders in
-                // one digit): rank every member against all others with all
-                // 128 threads -- thread t its own bins 2t, 2t+1, scanning the
-                // 256 (digit, remainder) pairs 8 at a time (broadcast shared
-                // loads) -- instead of one member at a time (~40k cycles).
-                // Uniform across the chain's warps (B, nB, need come from the
-                // same shared data), so the barrier below is safe.
-                const int ka = 2 * t;
-                const double fa = cs->frac[ka], fb = cs->frac[ka + 1];
-                const bool ma = cs->dig[ka] == (uint8_t)B, mb = cs->dig[ka + 1] == (uint8_t)B;
-                int ra = 0, rb = 0;
-                if (ma || mb) {
-#pragma unroll 2
-                    for (int j8 = 0; j8 < 256; j8 += 8) {
-                        const uint2 dv = *reinterpret_cast<const uint2*>(cs->dig + j8);
-                        const double2* f2 = reinterpret_cast<const double2*>(cs->frac + j8);
-                        const double2 q0 = f2[0], q1 = f2[1], q2 = f2[2], q3 = f2[3];
-                        const double fj[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+                // one digit): each warp radix-selects through the next digits
+                // of the members' remainders in its own histogram
+                // (warp_crowded_pick, lpic_cdf.cuh) instead of ranking member
+                // by member (~40k cycles per such table).
+                double fr8[8];
+                const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
 #pragma unroll
-                        for (int u = 0; u < 8; u++) {
-                            const uint32_t d = ((u < 4 ? dv.x : dv.y) >> (8 * (u & 3))) & 0xFFu;
-                            const bool in = d == (uint32_t)B;
-                            ra += in && beats(fj[u], j8 + u, fa, ka);
-                            rb += in && beats(fj[u], j8 + u, fb, ka + 1);
-                        }
-                    }
-                }
-                if (ma && ra < need) atomicOr(cs->plus + (ka >> 5), 1u << (ka & 31));
-                if (mb && rb < need) atomicOr(cs->plus + ((ka + 1) >> 5), 1u << ((ka + 1) & 31));
-                chain_sync(bar);
-                bm |= (cs->plus[lane >> 2] >> (8 * (lane & 3))) & 0xFFu & mem;
+                for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr8[2 * u] = v.x; fr8[2 * u + 1] = v.y; }
+                bm |= warp_crowded_pick(fr8, mem, need, nB, cs->whist[w]);
             } else {
                 // exact ranks among the (few) members of B, frac desc / index asc
                 double fr[8];

@@ -330,10 +330,10 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
               float* trace_raw) {
     extern __shared__ __align__(128) unsigned char smem[];
     Tc2Smem* s = reinterpret_cast<Tc2Smem*>(smem);
-    __shared__ float lut[256];
     constexpr int TC = Taps<HH>::TC;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int v = tid; v < 256; v += blockDim.x) lut[v] = __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f);
+    for (int l = 0; l < w.nl; l++)
+        for (int c = tid; c < TC_NMAX; c += blockDim.x) s->bias[l][c] = c < w.N[l] ? w.bias[l][c] : 0.0f;
     if (warp == TC2_MMA_WARP) umma::tmem_alloc(&s->tmem, 512);
     if (tid == 0) {
         for (int i = 0; i < 3; i++) { tc2_mbar_init(&s->wfull[i], 1); tc2_mbar_init(&s->wfree[i], 1); }
@@ -391,7 +391,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                 float x[TC];
                 if (valid) {
                     const int32_t ij = __ldg(order + n);
-                    gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+                    gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, NormU8(), x, LdgU8());
                 } else {
 #pragma unroll
                     for (int q = 0; q < TC; q++) x[q] = 0.0f;
@@ -406,30 +406,24 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
             for (int l = 0; l < w.nl; l++) {
                 const bool last = l == w.nl - 1;
                 const int Nl = w.N[l], Knext = last ? 0 : w.K[l + 1];
-                const float* bias = w.bias[l];
+                const float* bias = s->bias[l];
                 tc_mbar_wait(&s->dfull[t], dcnt & 1u);
                 dcnt++;
                 umma::fence_after();
-                for (int c0 = 64 * hf; c0 < Nl && c0 < 64 * hf + 64; c0 += 32) {
-                    float bv[32];
+                for (int c0 = 64 * hf; c0 < Nl && c0 < 64 * hf + 64; c0 += 16) {
+                    float d0[16], d1[16];
+                    umma::tmem_ld16(dcol + lane_off + (uint32_t)c0, d0);
+                    umma::tmem_ld16(dcol + lane_off + (uint32_t)(TC_NMAX + c0), d1);
+                    float y[16];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) {             // (issued ahead of the TMEM loads)
-                        const float4 q4 = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
-                        bv[i] = q4.x; bv[i + 1] = q4.y; bv[i + 2] = q4.z; bv[i + 3] = q4.w;
-                    }
-                    float d0[32], d1[32];
-                    umma::tmem_ld32(dcol + lane_off + (uint32_t)c0, d0);
-                    umma::tmem_ld32(dcol + lane_off + (uint32_t)(TC_NMAX + c0), d1);
-                    float y[32];
-#pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const float v = __fadd_rn(__fadd_rn(d0[i], __fmul_rn(d1[i], 4.8828125e-4f)), bv[i]);
+                    for (int i = 0; i < 16; i++) {
+                        const float v = __fadd_rn(__fadd_rn(d0[i], __fmul_rn(d1[i], 4.8828125e-4f)), bias[c0 + i]);
                         y[i] = last ? v : (v >= 0.0f ? v : __fmul_rn(0.01f, v));
                     }
                     if (last) {
                         if (row) {
 #pragma unroll
-                            for (int i = 0; i < 32; i++)
+                            for (int i = 0; i < 16; i++)
                                 if (c0 + i < w.M) {
                                     row[c0 + i] = y[i];
                                     finite &= isfinite(y[i]);
@@ -437,7 +431,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                                 }
                         }
                     } else if (c0 < Knext) {
-                        tc2_store_split(a_hi, a_lo, r, c0, Knext, y, (Knext - c0) >= 32 ? 4 : (Knext - c0) >> 3);
+                        tc2_store_split16(a_hi, a_lo, r, c0, Knext, y);
                     }
                 }
                 umma::fence_before();
@@ -1418,7 +1412,7 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
                 for (int k0 = 0; k0 < Ks[l]; k0 += TC2_KB) {
                     bl.push_back(l); bk0.push_back(k0); bkb.push_back(Ks[l] - k0 < TC2_KB ? Ks[l] - k0 : TC2_KB);
                 }
-            if ((int)bl.size() <= TC2_MAXB && m->tc_ok) {
+            if ((int)bl.size() <= TC2_MAXB && nl <= TC2_MAXL && m->tc_ok) {
                 std::vector<size_t> boff2(bl.size());
                 size_t tot2 = 0;
                 for (size_t b = 0; b < bl.size(); b++) { boff2[b] = tot2; tot2 += (size_t)2 * Ns[bl[b]] * bkb[b] * 2; }

@@ -34,6 +34,7 @@ namespace lpic {
 constexpr int TC2_KB = 64;                                  // K columns per weight block
 constexpr int TC2_WBLK = 2 * TC_NMAX * TC2_KB * 2;          // bytes of one block (hi | lo), 32 KB
 constexpr int TC2_MAXB = 2 * TC_MAXL;                       // blocks per network pass
+constexpr int TC2_MAXL = 5;                                 // layers (L <= 5: the reference configs; else k_enc_net_tc)
 constexpr int TC2_MMA_WARP = 16, TC2_LOAD_WARP = 17;
 constexpr int TC2_THREADS = 32 * 18;           // 16 epilogue warps, MMA issue, weight loader
 
@@ -51,6 +52,7 @@ struct Tc2Smem {
     alignas(128) unsigned char a_hi[2][TC_M * TC_KMAX * 2];
     alignas(128) unsigned char a_lo[2][TC_M * TC_KMAX * 2];
     alignas(128) unsigned char w[3][TC2_WBLK];
+    float bias[TC2_MAXL][TC_NMAX];                          // the layers' biases (broadcast reads)
     alignas(8) uint64_t wfull[3], wfree[3], aready[2], dfull[2];
     uint32_t tmem;
 };
@@ -69,6 +71,26 @@ __device__ __forceinline__ void tc2_store_split(unsigned char* a_hi, unsigned ch
 #pragma unroll
     for (int g = 0; g < 4; g++) {
         if (g >= ng) break;
+        __half2 h[4], l[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float a = y[8 * g + 2 * i], b = y[8 * g + 2 * i + 1];
+            const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+            h[i] = __halves2half2(ha, hb);
+            l[i] = __halves2half2(__float2half_rn((a - __half2float(ha)) * 2048.0f),
+                                  __float2half_rn((b - __half2float(hb)) * 2048.0f));
+        }
+        const uint32_t off = umma::op_offset(r, c0 + 8 * g, K);
+        *reinterpret_cast<uint4*>(a_hi + off) = *reinterpret_cast<uint4*>(h);
+        *reinterpret_cast<uint4*>(a_lo + off) = *reinterpret_cast<uint4*>(l);
+    }
+}
+
+// the same for a 16-column chunk (two groups of 8)
+__device__ __forceinline__ void tc2_store_split16(unsigned char* a_hi, unsigned char* a_lo, int r, int c0, int K,
+                                                  const float (&y)[16]) {
+#pragma unroll
+    for (int g = 0; g < 2; g++) {
         __half2 h[4], l[4];
 #pragma unroll
         for (int i = 0; i < 4; i++) {

@@ -27,6 +27,11 @@ __host__ __device__ __forceinline__ void sched_rows(int64_t t, int a, int H, int
 // byte loaders for gather_u8: read-only path (encoder) / L2, bypassing L1
 // (decoder producer, which reads pixels another SM has just written)
 struct LdgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldg(p); } };
+// normalize_value computed in place of a table lookup (the same two IEEE
+// operations the tables are built with, network.py:172-177)
+struct NormU8 {
+    __device__ float operator[](uint32_t v) const { return __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f); }
+};
 struct LdcgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldcg(p); } };
 
 template <int HH> struct Taps {
@@ -43,9 +48,9 @@ template <int HH> struct Taps {
 // diagonal mode the taps (-1,1), (-1,2), (-2,2) are redirected to (i-2,j+1)
 // or the first decoded in-bounds tap (schedules.py:114-131; h = 2 only).
 // LOAD(ptr) abstracts the load (L1-bypassing in the decoder).
-template <int HH, typename Load>
+template <int HH, typename Load, typename Lut>
 __device__ __forceinline__ void gather_u8(const uint8_t* im, int H, int W, int i, int j, int mode,
-                                          const float* lut, float (&x)[Taps<HH>::TC], Load load) {
+                                          const Lut& lut, float (&x)[Taps<HH>::TC], Load load) {
     constexpr int T = Taps<HH>::T;
 #pragma unroll
     for (int k = 0; k < T; k++) {
