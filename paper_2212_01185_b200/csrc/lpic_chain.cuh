@@ -21,8 +21,9 @@
 //      deficit-th largest remainder (suffix sums by a warp scan); if B is
 //      split (it holds ~1-2 bins), its members are ranked exactly
 //      (remainder desc, index asc == the reference's stable argsort of
-//      f - v, kernels.py:286-290); cdf = prefix of m + prefix of the +1s;
-//      symbol search against the target.
+//      f - v, kernels.py:286-290; warp_rank_pick, or warp_crowded_pick's
+//      radix levels first for > 32 members); cdf = prefix of m + prefix of
+//      the +1s; symbol search against the target.
 //
 // The arithmetic is bin-for-bin identical to the warp builder (lpic_cdf.cuh
 // warp_table), so encoder and decoder agree (scripts/ubench_chain.cu checks
@@ -337,42 +338,20 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             const uint32_t mem = bits8(__vcmpeq4(dg.x, Bx4), __vcmpeq4(dg.y, Bx4));
             if (need == nB) {
                 bm |= mem;
-            } else if (nB > 24) {
-                // Crowded bucket (near-flat mixtures put most remainders in
-                // one digit): each warp radix-selects through the next digits
-                // of the members' remainders in its own histogram
-                // (warp_crowded_pick, lpic_cdf.cuh) instead of ranking member
-                // by member (~40k cycles per such table).
+            } else {
                 double fr8[8];
                 const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
 #pragma unroll
                 for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr8[2 * u] = v.x; fr8[2 * u + 1] = v.y; }
-                bm |= warp_crowded_pick(fr8, mem, need, nB, cs->whist[w]);
-            } else {
-                // exact ranks among the (few) members of B, frac desc / index asc
-                double fr[8];
-                const double2* f2 = reinterpret_cast<const double2*>(cs->frac) + 4 * lane;
-#pragma unroll
-                for (int u = 0; u < 4; u++) { const double2 v = f2[u]; fr[2 * u] = v.x; fr[2 * u + 1] = v.y; }
-                int rank[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) rank[q] = 0;
-                uint32_t lanes = __ballot_sync(0xffffffffu, mem != 0);
-                while (lanes) {
-                    const int src = __ffs(lanes) - 1;
-                    lanes &= lanes - 1;
-                    uint32_t qs = __shfl_sync(0xffffffffu, mem, src);
-                    while (qs) {
-                        const int q2 = __ffs(qs) - 1;
-                        qs &= qs - 1;
-                        const int j = 8 * src + q2;
-                        const double f = cs->frac[j];
-#pragma unroll
-                        for (int q = 0; q < 8; q++) rank[q] += beats(f, j, fr[q], 8 * lane + q);
-                    }
+                if (nB > 32) {
+                    // Crowded bucket (near-flat mixtures put most remainders in
+                    // one digit): radix select on the members' remainder bits
+                    // in the warp's own histogram (warp_crowded_pick, lpic_cdf.cuh)
+                    bm |= warp_crowded_pick(fr8, mem, need, nB, cs->whist[w]);
+                } else {
+                    // exact ranks among the members of B (frac desc / index asc)
+                    bm |= warp_rank_pick(fr8, mem, need, nB, cs->whist[w]);
                 }
-#pragma unroll
-                for (int q = 0; q < 8; q++) bm |= (uint32_t)(((mem >> q) & 1) && rank[q] < need) << q;
             }
         }
     }

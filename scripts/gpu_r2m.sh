@@ -1,0 +1,8 @@
+# iteration m: RcDecoder + L1 prefetch (window decoder reverted), analytic
+# tail window in the encoder's warp PMF, list ranking.
+cd $GRAFT_REPO_ROOT
+D=gpurun_out/r2m; mkdir -p $D
+timeout 180 ./scripts/ubench_chain > $D/ubench_chain.log 2>&1; echo "chain rc $?"; grep -E "cycles per table|TOTAL" $D/ubench_chain.log
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x > $D/pytest_parity.log 2>&1; echo "parity tests rc $?"; tail -3 $D/pytest_parity.log
+for i in 1 2; do timeout 900 python bench.py --steps 3 --no-cpu-baseline --parity-images 1 > $D/bench_default_$i.log 2>&1; echo "bench rc $?"; grep '^{' $D/bench_default_$i.log | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('dec', d['value'], 'enc', d['encode']['value'], 'chain', d.get('chain',{}).get('frac'), 'parity', d.get('parity',{}).get('byte_identical'))"; done
+timeout 900 python bench.py --weights fitted --steps 2 --no-cpu-baseline --parity-images 1 > $D/bench_fitted.log 2>&1; echo "fitted bench rc $?"; grep '^{' $D/bench_fitted.log | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('dec', d['value'], 'enc', d['encode']['value'], 'bpsp', d['bpsp'], 'parity', d.get('parity',{}).get('byte_identical'))"

@@ -4,6 +4,7 @@ bit-exact (uint32 view) with the reference's canonical float32 order."""
 
 import ctypes as C
 import hashlib
+import math
 import os
 
 import numpy as np
@@ -660,3 +661,55 @@ def test_gpu_flat_mixtures_match_oracle(P, oracle_mod):
         c = P.encode(img, w, cfg, mode)
         assert c.payload == oracle_mod.encode(ow, img, mode), mode
         assert np.array_equal(P.decode(c, w, cfg), img), mode
+
+
+def _quantize_from_pmf(pmf):
+    """kernels._quantized_cdf (kernels.py:272-293) from a given PMF row, with
+    the GPU's exact 2^-62 fixed-point total (lpic_cdf.cuh fx_*): floors,
+    deficit to the largest remainders (stable argsort of f - v, ties to the
+    lower index), prefix sum.  Pure integer/IEEE-double work, so it checks the
+    device selection bit for bit whatever the PMF values are."""
+    fx = sum(int(np.floor(float(p) * 2.0 ** 62)) for p in pmf)
+    total = float(fx) * 2.0 ** -62
+    scale = 65280.0 / total
+    v = pmf * scale
+    f = np.minimum(np.floor(v), 65280.0)
+    m = f.astype(np.int64) + 1
+    deficit = 65536 - int(m.sum())
+    if deficit > 0:
+        order = np.argsort(f - v, kind="stable")
+        m[order[:deficit]] += 1
+    return np.concatenate([[0], np.cumsum(m)])
+
+
+def test_gpu_selection_crowded_and_ties_exact(P):
+    """Deficit selection on its worst cases, checked exactly from the GPU's own
+    PMF: near-flat mixtures (log-scales e^5..e^7: ~250 remainders share the
+    first digits, the crowded-bucket radix path), symmetric single Gaussians
+    (exactly equal remainder pairs, ties to the lower index) and ordinary
+    mixtures, through lpic_quantized_cdf (warp builder)."""
+    import torch
+    from paper_2212_01185_b200 import _native
+    L = _native.load()
+    rng = np.random.default_rng(77)
+    rows = []
+    for _ in range(600):                                      # near-flat, 3 components
+        rows.append((rng.dirichlet([1, 1, 1]), rng.uniform(-0.9, 0.9, 3), np.exp(rng.uniform(5.0, 7.0, 3))))
+    for _ in range(200):                                      # symmetric: exact ties
+        s0 = math.exp(rng.uniform(-3.0, 7.0))
+        rows.append((np.array([1.0, 0.0, 0.0]), np.array([0.0, 0.3, -0.3]), np.array([s0, 1.0, 1.0])))
+    for _ in range(200):                                      # flat + one peaked component
+        rows.append((np.array([0.98, 0.015, 0.005]), np.array([0.0, rng.uniform(-1, 1), 0.2]),
+                     np.array([1096.6, math.exp(rng.uniform(-6, -2)), 800.0])))
+    pi = np.array([r[0] for r in rows], np.float64)
+    mu = np.array([r[1] for r in rows], np.float64)
+    s = np.array([r[2] for r in rows], np.float64)
+    N, K = pi.shape
+    t = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (pi, mu, s)]
+    cdf = torch.empty((N, 257), dtype=torch.int32, device="cuda")
+    pmf = torch.empty((N, 256), dtype=torch.float64, device="cuda")
+    _native.check(L.lpic_quantized_cdf(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), N, K, 0, cdf.data_ptr(),
+                                       pmf.data_ptr(), None, _native.stream_ptr()), "quantized_cdf")
+    cdf, pmf = cdf.cpu().numpy().astype(np.int64), pmf.cpu().numpy()
+    bad = [n for n in range(N) if not np.array_equal(cdf[n], _quantize_from_pmf(pmf[n]))]
+    assert not bad, f"{len(bad)} of {N} tables differ from the exact selection (rows {bad[:8]})"
