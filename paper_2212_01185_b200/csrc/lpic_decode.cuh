@@ -21,6 +21,13 @@
 // and its work is off the critical path.  The cluster guarantees both CTAs
 // are co-resident, so the cross-CTA spin-waits cannot deadlock.
 #pragma once
+// In-situ chain phase profile (A/B builds only: -DLPIC_DEC_PROF): the chain
+// builder's CHP timestamps (lpic_chain.cuh) accumulate into s_chp and stream
+// 0's consumer appends them to the decoder timeline buffer.
+#ifdef LPIC_DEC_PROF
+__shared__ long long s_chp[16];
+#define LPIC_CHAIN_PROF s_chp
+#endif
 #include "lpic_cdf.cuh"
 #include "lpic_chain.cuh"
 #include "lpic_net.cuh"
@@ -422,13 +429,21 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
         return;
     }
     const int ct = tid & (CH_THREADS - 1);            // chain-local thread
+#ifdef LPIC_DEC_PROF
+    if (ct < 16) s_chp[ct] = 0;
+    chain_sync(bar);
+#endif
     RcDecoder dec;
     dec.init(P.payload + P.offs[img], P.lens[img]);
     ChainSmem* ch = &cs->ch;
     uint32_t avail = 0;                               // records known to be in their slots
     for (int64_t n = 0; n < N; n++) {
         const int s = (int)(n % DEC_SLOTS);
+#ifdef LPIC_DEC_TIMELINE
         unsigned long long* dbg = (P.dbg && img == 0) ? P.dbg + 4 * (int64_t)P.n_chunks + 12 * n : nullptr;
+#else
+        constexpr unsigned long long* dbg = nullptr;  // (per-pixel stamps: timeline builds only)
+#endif
         if (dbg && ct == 0) dbg[0] = gtimer();
         if ((int64_t)avail <= n) {
             // the loader publishes completed copies lazily; if it has not yet
@@ -444,7 +459,16 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
         int32_t* trow = P.trace_cdf ? P.trace_cdf + ((int64_t)img * N + n) * 3 * 257 : nullptr;
         // ---- red: table precomputed by the producer; every warp searches it
         uint64_t r;
-        uint32_t target = dec.target(r);
+#ifdef LPIC_RED_QUOTIENT
+        const uint32_t target = dec.target(r);
+        auto le = [&](uint32_t c) { return c <= target; };
+#else
+        // (no quotient on this serial step: cdf_k <= min(code // r, 65535)
+        // <=> cdf_k * r <= code, as every cdf_k < 65536 -- coder.py:100-104)
+        r = dec.range >> 16;
+        const uint64_t code = dec.code;
+        auto le = [&](uint32_t c) { return (uint64_t)c * r <= code; };
+#endif
         int sr;
         uint32_t red_start, red_width;
         {
@@ -452,7 +476,7 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
             const uint32_t e[4] = {v.x, v.y, v.z, v.w};
             int c = 0;
 #pragma unroll
-            for (int q = 0; q < 4; q++) c += ((e[q] & 0xFFFFu) <= target) + ((e[q] >> 16) <= target);
+            for (int q = 0; q < 4; q++) c += le(e[q] & 0xFFFFu) + le(e[q] >> 16);
             sr = __reduce_add_sync(0xffffffffu, c) - 1;
             const uint32_t rs = rv.red[sr];
             const uint32_t re = sr == 255 ? 65536u : (uint32_t)rv.red[sr + 1];
@@ -485,7 +509,11 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
         if (dbg && ct == 0) dbg[8] = clock64();
         if (ct == 0) {                                // (slot s was last read before the blue table's barrier A)
             mbar_arrive(&cs->empty[s]);
-            while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ <= n) __nanosleep(20);
+            // publisher back-pressure: the queue holds DEC_PUBQ pixels, so
+            // checking every DEC_PUBQ / 2 pixels for half a queue of room
+            // keeps the load off most pixels' critical path
+            if ((n & (DEC_PUBQ / 2 - 1)) == 0)
+                while ((int64_t)ld_volatile_smem(&cs->pub_done) + DEC_PUBQ / 2 <= n) __nanosleep(20);
             const unsigned long long v = ((unsigned long long)(n & 0xFF) << 56) |
                                          ((unsigned long long)((uint32_t)sr | ((uint32_t)sg << 8) | ((uint32_t)sb << 16)) << 32) |
                                          (uint32_t)rv.ij;
@@ -494,6 +522,9 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
         }
     }
     if (ct == 0 && dec.status) atomicOr(P.status + img, dec.status);
+#ifdef LPIC_DEC_PROF
+    if (P.dbg && img == 0 && ct < 16) P.dbg[4 * (int64_t)P.n_chunks + 12 * N + ct] = (unsigned long long)s_chp[ct];
+#endif
 }
 
 // NT = 256: one stream per cluster (latency; up to 255 registers per

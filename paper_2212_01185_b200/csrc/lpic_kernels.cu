@@ -1483,8 +1483,9 @@ int lpic_last_launch_count(const lpic_model_t* m) { return m ? m->launches : 0; 
 
 /* Diagnostics (not part of include/lpic_b200.h): record a globaltimer
  * timeline of stream 0 of the next decode into d_buf (4 stamps per producer
- * chunk followed by 3 per pixel); pass NULL to disable.  Returns the number
- * of producer chunks of the last decode geometry. */
+ * chunk followed by 12 per pixel; the per-pixel stamps only in builds with
+ * -DLPIC_DEC_TIMELINE, scripts/ab_build.py); pass NULL to disable.  Returns
+ * the number of producer chunks of the last decode geometry. */
 int lpic_decode_debug(lpic_model_t* m, unsigned long long* d_buf) {
     if (!m) return -1;
     m->d_dbg = d_buf;

@@ -79,6 +79,7 @@ struct RcDecoder {
     int64_t len, pos;
     int virt;
     int status;
+    uint32_t nb;      // advance_bf: bytes pos, pos+1 (0 past the end), loaded one advance ahead
 
     __device__ __forceinline__ int next_byte() {           // coder.py:86-96
         if (pos < len) return __ldg(data + pos++);
@@ -89,6 +90,10 @@ struct RcDecoder {
     __device__ __forceinline__ void init(const uint8_t* d, int64_t n) {
         data = d; len = n; pos = 0; virt = 0; status = ST_OK; range = RC_TOP - 1; code = 0;
         for (int k = 0; k < 6; k++) code = (code << 8) | (uint64_t)next_byte();
+        prefetch2();
+    }
+    __device__ __forceinline__ void prefetch2() {
+        nb = (pos < len ? (uint32_t)__ldg(data + pos) : 0u) | ((pos + 1 < len ? (uint32_t)__ldg(data + pos + 1) : 0u) << 8);
     }
     // target = min(code // r, 65535) (coder.py:100-103), exact: a float64
     // quotient estimate (code < 2^48, 2^24 <= r < 2^32, so q < 2^24 and the
@@ -116,22 +121,22 @@ struct RcDecoder {
     }
     // The same, branch-free (so it can be scheduled into the shadow of other
     // work): r >= 2^24 and width >= 1 bound the renormalisation to two bytes.
+    // The two bytes it may consume were loaded by the previous advance
+    // (prefetch2), so no global load sits on the decoder chain's critical
+    // path (in situ, r2q: the advance + target cost ~640 cycles per table
+    // while the byte loads were issued inside it; ~50 with L1-resident data).
     __device__ __forceinline__ void advance_bf(uint64_t r, uint32_t start, uint32_t width) {
         code -= r * start;
         const uint64_t rg = r * width;
         const bool n1 = rg < RC_BOTTOM, n2 = rg < (RC_BOTTOM >> 8);
         const bool in0 = pos < len, in1 = pos + 1 < len;
-        // pull the line ~64 bytes (~20 pixels) ahead into L1, so the byte
-        // loads below -- on the chain's critical path -- never miss to L2
-        // (ncu r2k: 6% of the chain's stall samples were those misses)
-        if (len > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + (pos + 64 < len ? pos + 64 : len - 1)));
-        const uint64_t b0 = (n1 && in0) ? (uint64_t)__ldg(data + pos) : 0ull;
-        const uint64_t b1 = (n2 && in1) ? (uint64_t)__ldg(data + pos + 1) : 0ull;
+        const uint64_t b0 = nb & 0xFFu, b1 = (nb >> 8) & 0xFFu;   // (0 past the end)
         virt += (int)(n1 && !in0) + (int)(n2 && !in1);        // bytes past the end read as 0
         status |= virt > 3 ? ST_CORRUPT : 0;                 // coder.py:94-95
         code = n2 ? (((code << 16) & RC_MASK) | (b0 << 8) | b1) : (n1 ? (((code << 8) & RC_MASK) | b0) : code);
         range = n2 ? rg << 16 : (n1 ? rg << 8 : rg);
         pos += (int64_t)n1 + (int64_t)n2;
+        prefetch2();                                         // consumed by the next advance, a table later
     }
 };
 

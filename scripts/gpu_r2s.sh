@@ -1,0 +1,9 @@
+# iteration s: chain symbol search by multiply-compare (A/B vs quotient build)
+cd $GRAFT_REPO_ROOT
+D=gpurun_out/r2s; mkdir -p $D
+timeout 180 ./scripts/ubench_chain > $D/ubench_chain.log 2>&1; echo "chain rc $?"; grep -E "cycles per table|TOTAL" $D/ubench_chain.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > $D/pytest_parity.log 2>&1; echo "tests rc $?"; tail -2 $D/pytest_parity.log
+for v in main quot main quot; do
+  if [ $v = main ]; then LIB=""; else LIB="LPIC_LIB=paper_2212_01185_b200/ab/$v.so"; fi
+  env $LIB timeout 300 python scripts/dec_time.py kaiming 3 2>&1 | tail -1
+done | tee $D/dec_ab.txt
