@@ -114,6 +114,9 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
     const int k0 = 2 * t;                                   // bins k0, k0 + 1
     uint32_t target = 0;
     CHP0;
+#ifdef LPIC_TGT_EARLY
+    target = chain_target(tgt);          // (A/B: issued ahead of the Phi phase)
+#endif
 
     double p0 = 0.0, p1 = 0.0;
     if constexpr (F32) {
@@ -139,7 +142,9 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             cs->wedgeq[w][q] = qb[q]; cs->wedgep[w][q] = pb[q];
         }
     }
+#ifndef LPIC_TGT_EARLY
     target = chain_target(tgt);
+#endif
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);
@@ -211,7 +216,9 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
             cs->wedge[w][q] = cur[2 * q + 1];
         }
     }
+#ifndef LPIC_TGT_EARLY
     target = chain_target(tgt);
+#endif
     CHP(0);
     chain_sync(bar);                                                                        // E
     CHP(1);

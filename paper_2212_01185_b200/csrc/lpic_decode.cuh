@@ -42,6 +42,9 @@ constexpr int DEC_THREADS = 384;        // (S = 2) consumer: S x (4 chain warps)
                                         // producer: net_tile on 256, the rest only join its barriers
 constexpr int DEC_SLOTS = 8;
 constexpr int DEC_PUBQ = 32;            // decoded pixels queued for the publisher warp
+#ifndef LPIC_AUX_SLEEP
+#define LPIC_AUX_SLEEP 256               // loader / publisher poll interval (ns): they share schedulers with chain warps
+#endif
 
 struct DecParams {
     NetDev w;
@@ -388,11 +391,11 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
             for (int64_t n = 0; n < N; n++) {
                 const int s = (int)(n % DEC_SLOTS);
                 if (n >= DEC_SLOTS) {
-                    while (!mbar_test(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1))) { publish(n); __nanosleep(256); }
+                    while (!mbar_test(&cs->empty[s], (uint32_t)(((n / DEC_SLOTS) - 1) & 1))) { publish(n); __nanosleep(LPIC_AUX_SLEEP); }
                 }
                 const uint32_t* fl = flags + (n & (P.ring_size - 1));
                 uint32_t ns = 32;
-                while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { publish(n); __nanosleep(ns); ns = ns < 256 ? ns * 2 : 256; }
+                while (ld_relaxed_u32(fl) != (uint32_t)(n + 1)) { publish(n); __nanosleep(ns); ns = ns < LPIC_AUX_SLEEP ? ns * 2 : LPIC_AUX_SLEEP; }
                 // acquire (pairs with the producer's st.release of the flag), then
                 // order the generic-proxy view before the bulk copy's async proxy
                 fence_acq_rel_gpu();
@@ -402,7 +405,7 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
                          (uint32_t)P.rec_bytes, &cs->full[s]);
                 publish(n + 1);
             }
-            while (done < N) { publish(N); __nanosleep(256); }
+            while (done < N) { publish(N); __nanosleep(LPIC_AUX_SLEEP); }
         }
         return;
     }
@@ -420,7 +423,7 @@ __device__ __forceinline__ void dec_consumer(const DecParams& P, int img0, unsig
                     px[0] = (uint8_t)rgb; px[1] = (uint8_t)(rgb >> 8); px[2] = (uint8_t)(rgb >> 16);
                     got++;
                 }
-                if (got == pub) { __nanosleep(200); continue; }
+                if (got == pub) { __nanosleep(LPIC_AUX_SLEEP); continue; }
                 pub = got;
                 *(volatile uint32_t*)&cs->pub_done = (uint32_t)pub;
                 st_release_u32(P.progress + img, (uint32_t)pub);

@@ -26,4 +26,7 @@ with ThreadPoolExecutor(max_workers=len(redo)) as ex:
 objs += [os.path.join(B.OBJDIR, s.replace(".cu", ".o")) for s in B.SOURCES if s not in redo]
 so = os.path.join(out, f"{name}.so")
 subprocess.run([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", so], check=True)
+for o in objs:                       # (keep the gpurun snapshot small: variant objects are not reused)
+    if os.path.basename(o).startswith("ab_"):
+        os.remove(o)
 print(so)
