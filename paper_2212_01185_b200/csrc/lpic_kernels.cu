@@ -336,7 +336,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
         for (int c = tid; c < TC_NMAX; c += blockDim.x) s->bias[l][c] = c < w.N[l] ? w.bias[l][c] : 0.0f;
     if (warp == TC2_MMA_WARP) umma::tmem_alloc(&s->tmem, 512);
     if (tid == 0) {
-        for (int i = 0; i < 3; i++) { tc2_mbar_init(&s->wfull[i], 1); tc2_mbar_init(&s->wfree[i], 1); }
+        for (int i = 0; i < TC2_SLOTS; i++) { tc2_mbar_init(&s->wfull[i], 1); tc2_mbar_init(&s->wfree[i], 1); }
         for (int t = 0; t < 2; t++) { tc2_mbar_init(&s->aready[t], 256); tc2_mbar_init(&s->dfull[t], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -350,8 +350,8 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
         if (lane == 0) {
             const int64_t nblocks = my_pairs * w.nb;
             for (int64_t g = 0; g < nblocks; g++) {
-                const int slot = (int)(g % 3), b = (int)(g % w.nb);
-                if (g >= 3) tc_mbar_wait(&s->wfree[slot], (uint32_t)(((g / 3) - 1) & 1));
+                const int slot = (int)(g % TC2_SLOTS), b = (int)(g % w.nb);
+                if (g >= TC2_SLOTS) tc_mbar_wait(&s->wfree[slot], (uint32_t)(((g / TC2_SLOTS) - 1) & 1));
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                              ::"r"(umma::smem_addr(&s->wfull[slot])), "r"((uint32_t)w.blk_bytes[b]) : "memory");
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -360,7 +360,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
             }
         }
     } else if (warp == TC2_MMA_WARP) {                        // MMA issue (whole warp, elected lane)
-        uint32_t acnt[2] = {0u, 0u}, wcnt[3] = {0u, 0u, 0u};
+        uint32_t acnt[2] = {0u, 0u}, wcnt[TC2_SLOTS] = {};
         int64_t g = 0;
         for (int64_t p = 0; p < my_pairs; p++) {
             for (int l = 0; l < w.nl; l++) {
@@ -383,30 +383,41 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
         unsigned char* a_hi = s->a_hi[t];
         unsigned char* a_lo = s->a_lo[t];
         uint32_t dcnt = 0;
+        // the first layer's operand (all of K0) of row r of `tile`
+        auto gather = [&](int64_t tile, float (&x)[TC]) {
+            const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + r;
+            if (tile < total && n < N) {
+                const int32_t ij = __ldg(order + n);
+                gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, NormU8(), x, LdgU8());
+            } else {
+#pragma unroll
+                for (int q = 0; q < TC; q++) x[q] = 0.0f;
+            }
+        };
         for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
             const int64_t tile = 2 * p + t;
             const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + r;
             const bool valid = tile < total && n < N;
-            if (hf == 0) {                                    // the first layer's operand (all of K0)
+            if (hf == 0 && p == (int64_t)blockIdx.x) {        // the CTA's first pair: gathered here
                 float x[TC];
-                if (valid) {
-                    const int32_t ij = __ldg(order + n);
-                    gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, NormU8(), x, LdgU8());
-                } else {
-#pragma unroll
-                    for (int q = 0; q < TC; q++) x[q] = 0.0f;
-                }
+                gather(tile, x);
                 tc2_store_input<TC>(a_hi, a_lo, r, x, w.K[0]);
                 umma::fence_async_smem();
             }
+            // (later pairs: the column-half-1 warps gathered this operand during
+            // the previous pair's last layer, where they have no columns --
+            // the taps' global-load latency overlaps that layer's MMAs)
             umma::fence_before();
             tc2_arrive(&s->aready[t]);
             float* row = valid ? raw_out + (img * N + n) * w.M : nullptr;
             bool finite = true;
+            const bool pre = hf == 1 && p + gridDim.x < pairs;  // this warp prepares the next pair's operand
             for (int l = 0; l < w.nl; l++) {
                 const bool last = l == w.nl - 1;
                 const int Nl = w.N[l], Knext = last ? 0 : w.K[l + 1];
                 const float* bias = s->bias[l];
+                float xn[TC];
+                if (last && pre) gather(2 * (p + gridDim.x) + t, xn);   // loads in flight during the MMAs
                 tc_mbar_wait(&s->dfull[t], dcnt & 1u);
                 dcnt++;
                 umma::fence_after();
@@ -432,6 +443,11 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                     } else if (c0 < Knext) {
                         tc2_store_split16(a_hi, a_lo, r, c0, Knext, y);
                     }
+                }
+                if (last && pre) {
+                    // this tile's last MMAs have completed (dfull): its A operand is free
+                    tc2_store_input<TC>(a_hi, a_lo, r, xn, w.K[0]);
+                    umma::fence_async_smem();
                 }
                 umma::fence_before();
                 if (!last) {
@@ -1404,7 +1420,7 @@ int lpic_model_create(const float* masked_w, const float* masked_b, const float*
                 }
                 m->tc_ok = true;
             }
-            // the same weights as 64-column K blocks for the pipelined encoder
+            // the same weights as TC2_KB-column K blocks for the pipelined encoder
             // network (k_enc_net_tc2): per block W_hi (N x Kb) | W_lo (N x Kb)
             std::vector<int> bl, bk0, bkb;
             for (int l = 0; l < nl; l++)

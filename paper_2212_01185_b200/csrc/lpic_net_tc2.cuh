@@ -33,6 +33,7 @@ namespace lpic {
 
 constexpr int TC2_KB = 64;                                  // K columns per weight block
 constexpr int TC2_WBLK = 2 * TC_NMAX * TC2_KB * 2;          // bytes of one block (hi | lo), 32 KB
+constexpr int TC2_SLOTS = 3;                                // weight ring slots (96 KB; 6 x 16 KB measured 9% slower, r3e)
 constexpr int TC2_MAXB = 2 * TC_MAXL;                       // blocks per network pass
 constexpr int TC2_MAXL = 5;                                 // layers (L <= 5: the reference configs; else k_enc_net_tc)
 constexpr int TC2_MMA_WARP = 16, TC2_LOAD_WARP = 17;
@@ -51,9 +52,9 @@ struct TcNet2Dev {
 struct Tc2Smem {
     alignas(128) unsigned char a_hi[2][TC_M * TC_KMAX * 2];
     alignas(128) unsigned char a_lo[2][TC_M * TC_KMAX * 2];
-    alignas(128) unsigned char w[3][TC2_WBLK];
+    alignas(128) unsigned char w[TC2_SLOTS][TC2_WBLK];
     float bias[TC2_MAXL][TC_NMAX];                          // the layers' biases (broadcast reads)
-    alignas(8) uint64_t wfull[3], wfree[3], aready[2], dfull[2];
+    alignas(8) uint64_t wfull[TC2_SLOTS], wfree[TC2_SLOTS], aready[2], dfull[2];
     uint32_t tmem;
 };
 
@@ -129,12 +130,12 @@ __device__ __forceinline__ bool tc2_elect_one() {
 // Executed by the whole MMA warp (so the descriptors stay warp-uniform, in
 // uniform registers); one elected lane issues each tcgen05 instruction.
 // gbase: global index (over the CTA's whole block stream) of the layer's
-// first block; the block's ring slot is its global index mod 3.  wcnt: uses
+// first block; the block's ring slot is its global index mod TC2_SLOTS.  wcnt: uses
 // of each slot so far (tile 0 waits for the copy, tile 1 then releases it).
 // Descriptors are formed once per block: advancing a K=16 slice adds
 // (offset >> 4) to the 14-bit start-address field.
 __device__ __forceinline__ void tc2_issue_layer(Tc2Smem* s, const TcNet2Dev& w, int t, int l, uint32_t tbase,
-                                                int64_t gbase, uint32_t (&wcnt)[3]) {
+                                                int64_t gbase, uint32_t (&wcnt)[TC2_SLOTS]) {
     const int N = w.N[l], K = w.K[l];
     const uint32_t idesc = umma::idesc_f16(TC_M, N);
     const uint32_t dcol = tbase + (uint32_t)(256 * t);
@@ -142,7 +143,7 @@ __device__ __forceinline__ void tc2_issue_layer(Tc2Smem* s, const TcNet2Dev& w, 
     const uint64_t dal = umma::smem_desc(umma::smem_addr(s->a_lo[t]), 128, (uint32_t)(K * 16));
     for (int j = 0; j < w.n_blk[l]; j++) {
         const int b = w.first_blk[l] + j;
-        const int slot = (int)((gbase + j) % 3);
+        const int slot = (int)((gbase + j) % TC2_SLOTS);
         if (t == 0) {                                       // first use of the block: wait for its copy
             tc_mbar_wait(&s->wfull[slot], wcnt[slot] & 1u);
             wcnt[slot]++;
