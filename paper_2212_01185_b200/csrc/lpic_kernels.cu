@@ -84,16 +84,19 @@ __device__ __forceinline__ void store_cdf_row(int32_t* row, const uint32_t start
 }
 
 // ---------------------------------------------------------------------------
-// encoder, stage 1: the network over 64-pixel tiles in coding order
-// (codec.py:116-145 + kernels.py:88-114): gather -> net_tile -> raw plane
+// encoder, stage 1: the network over 64-pixel RASTER runs (codec.py:116-145 +
+// kernels.py:88-114): gather -> net_tile -> raw plane rows in coding order
+// (inv: raster index -> coding index).  Adjacent lanes gather adjacent
+// pixels, so each tap load is one short run of bytes.
 // ---------------------------------------------------------------------------
 template <int CP, int HH>
 __global__ void __launch_bounds__(NT_THREADS)
-k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, const int32_t* __restrict__ order,
+k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, const int32_t* __restrict__ inv,
           int64_t N, float* __restrict__ raw_out, int32_t* status, float* trace_raw) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int TC = Taps<HH>::TC;
     __shared__ float lut[256];
+    __shared__ int32_t cidx[NT_TP];
     float* fb = reinterpret_cast<float*>(smem);
     NetTileBufs nb;
     net_tile_carve(fb, CP, TC, w.MT, w.MP, nb);
@@ -110,8 +113,9 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
         float x[TC];
         const int64_t n = n0 + tid;
         if (n < N) {
-            const int32_t ij = __ldg(order + n);
-            gather_u8<HH>(im, H, W, ij >> 16, ij & 0xFFFF, mode, lut, x, LdgU8());
+            const int i = (int)(n / W), j = (int)(n - (int64_t)i * W);
+            gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdgU8());
+            cidx[tid] = __ldg(inv + n);
         } else {
 #pragma unroll
             for (int q = 0; q < TC; q++) x[q] = 0.0f;
@@ -127,8 +131,8 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
         const int p = e / w.M, m = e - p * w.M;
         const float v = nb.raw[p * w.MP + m];
         finite &= isfinite(v);
-        raw_out[((int64_t)img * N + n0 + p) * w.M + m] = v;
-        if (trace_raw) trace_raw[((int64_t)img * N + n0 + p) * w.M + m] = v;
+        raw_out[((int64_t)img * N + cidx[p]) * w.M + m] = v;
+        if (trace_raw) trace_raw[((int64_t)img * N + cidx[p]) * w.M + m] = v;
     }
     if (!finite) atomicOr(status + img, LPIC_S_NONFINITE);
 }
@@ -326,7 +330,7 @@ struct RcPlanArgs {
 template <int HH>
 __global__ void __launch_bounds__(TC2_THREADS, 1)
 k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ images, int H, int W, int mode,
-              const int32_t* __restrict__ order, int64_t N, int n_img, float* __restrict__ raw_out, int32_t* status,
+              const int32_t* __restrict__ inv, int64_t N, int n_img, float* __restrict__ raw_out, int32_t* status,
               float* trace_raw) {
     extern __shared__ __align__(128) unsigned char smem[];
     Tc2Smem* s = reinterpret_cast<Tc2Smem*>(smem);
@@ -383,12 +387,16 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
         unsigned char* a_hi = s->a_hi[t];
         unsigned char* a_lo = s->a_lo[t];
         uint32_t dcnt = 0;
-        // the first layer's operand (all of K0) of row r of `tile`
+        // the first layer's operand (all of K0) of row r of `tile`.  Tiles are
+        // RASTER runs of 128 pixels (the network is per pixel; only the raw
+        // plane is in coding order, row inv[pixel]): a warp's 32 lanes gather
+        // 32 adjacent pixels, so every tap load is one 96-byte run instead of
+        // 32 rows apart (a coding-order run steps one row down per pixel)
         auto gather = [&](int64_t tile, float (&x)[TC]) {
             const int64_t img = tile / tiles_per, n = (tile - img * tiles_per) * TC_M + r;
             if (tile < total && n < N) {
-                const int32_t ij = __ldg(order + n);
-                gather_u8<HH>(images + img * N * 3, H, W, ij >> 16, ij & 0xFFFF, mode, NormU8(), x, LdgU8());
+                const int i = (int)(n / W), j = (int)(n - (int64_t)i * W);
+                gather_u8<HH>(images + img * N * 3, H, W, i, j, mode, NormU8(), x, LdgU8());
             } else {
 #pragma unroll
                 for (int q = 0; q < TC; q++) x[q] = 0.0f;
@@ -409,7 +417,8 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
             // the taps' global-load latency overlaps that layer's MMAs)
             umma::fence_before();
             tc2_arrive(&s->aready[t]);
-            float* row = valid ? raw_out + (img * N + n) * w.M : nullptr;
+            const int64_t cn = valid ? (int64_t)__ldg(inv + n) : 0;     // coding index of the row
+            float* row = valid ? raw_out + (img * N + cn) * w.M : nullptr;
             bool finite = true;
             const bool pre = hf == 1 && p + gridDim.x < pairs;  // this warp prepares the next pair's operand
             for (int l = 0; l < w.nl; l++) {
@@ -437,7 +446,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                                 if (c0 + i < w.M) {
                                     row[c0 + i] = y[i];
                                     finite &= isfinite(y[i]);
-                                    if (trace_raw) trace_raw[(img * N + n) * w.M + c0 + i] = y[i];
+                                    if (trace_raw) trace_raw[(img * N + cn) * w.M + c0 + i] = y[i];
                                 }
                         }
                     } else if (c0 < Knext) {
@@ -933,6 +942,7 @@ struct lpic_model {
     bool tc2_ok = false;
     // cached coding order per geometry
     int32_t* d_order = nullptr;
+    int32_t* d_inv = nullptr;          // raster index -> coding index (the FAST network's raster tiles)
     int ord_H = -1, ord_W = -1, ord_mode = -1;
     // workspace
     uint32_t* d_sw = nullptr; size_t sw_cap = 0;
@@ -1033,10 +1043,16 @@ int coding_order(lpic_model* m, int H, int W, int mode, cudaStream_t st) {
         sched_rows(t, a, H, W, lo, hi);
         for (int i = lo; i <= hi; i++) ord[(size_t)n++] = (i << 16) | (int)(t - (int64_t)a * i);
     }
+    std::vector<int32_t> inv((size_t)N);
+    for (int64_t k = 0; k < N; k++) inv[(size_t)((int64_t)(ord[(size_t)k] >> 16) * W + (ord[(size_t)k] & 0xFFFF))] = (int32_t)k;
     if (m->d_order) cudaFree(m->d_order);
+    if (m->d_inv) cudaFree(m->d_inv);
     m->d_order = nullptr;
+    m->d_inv = nullptr;
     CUDA_TRY(cudaMalloc(&m->d_order, sizeof(int32_t) * N));
+    CUDA_TRY(cudaMalloc(&m->d_inv, sizeof(int32_t) * N));
     CUDA_TRY(cudaMemcpyAsync(m->d_order, ord.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(m->d_inv, inv.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     m->ord_H = H; m->ord_W = W; m->ord_mode = mode;
     return 0;
@@ -1064,7 +1080,7 @@ int launch_enc_net_tc(lpic_model* m, const uint8_t* d_images, int n, int H, int 
         int sms2 = 148;
         cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, m->device);
         const unsigned grid2 = (unsigned)(pairs < sms2 ? pairs : sms2);
-        k_enc_net_tc2<HH><<<grid2, TC2_THREADS, smem2, st>>>(m->tcnet2, d_images, H, W, mode, m->d_order, N2, n, raw,
+        k_enc_net_tc2<HH><<<grid2, TC2_THREADS, smem2, st>>>(m->tcnet2, d_images, H, W, mode, m->d_inv, N2, n, raw,
                                                              d_status, tr);
         CUDA_TRY(cudaGetLastError());
         return 0;
@@ -1105,7 +1121,7 @@ template <int CP, int HH> struct EncodeRun {
             const size_t smem = net_tile_floats(CP, TC, m->MT, m->MP) * 4;
             if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
             dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
-            k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status, tr);
+            k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_inv, N, raw, d_status, tr);
             CUDA_TRY(cudaGetLastError());
         }
         const int64_t total = N * n;
@@ -1147,7 +1163,7 @@ template <int CP, int HH> struct NetRun {
         if (set_smem(k_enc_net<CP, HH>, smem)) return LPIC_E_CUDA;
         const int64_t N = (int64_t)H * W;
         dim3 grid((unsigned)((N + NT_TP - 1) / NT_TP), (unsigned)n);
-        k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_order, N, raw, d_status,
+        k_enc_net<CP, HH><<<grid, NT_THREADS, smem, st>>>(m->net, d_images, H, W, mode, m->d_inv, N, raw, d_status,
                                                           nullptr);
         CUDA_TRY(cudaGetLastError());
         return 0;
@@ -1473,7 +1489,7 @@ int lpic_model_destroy(lpic_model_t* m) {
     if (!m) return 0;
     DeviceGuard dg_(m->device);
     cudaFree(m->d_w);
-    cudaFree(m->d_order); cudaFree(m->d_sw); cudaFree(m->d_raw); cudaFree(m->d_img); cudaFree(m->d_pay);
+    cudaFree(m->d_order); cudaFree(m->d_inv); cudaFree(m->d_sw); cudaFree(m->d_raw); cudaFree(m->d_img); cudaFree(m->d_pay);
     cudaFree(m->d_pack); cudaFree(m->d_meta); cudaFree(m->d_status);
     cudaFree(m->d_step_off); cudaFree(m->d_chunks); cudaFree(m->d_ring); cudaFree(m->d_flags);
     cudaFree(m->d_progress);
