@@ -63,7 +63,7 @@ CONFIGS = {
 # capture of the same workload (algorithmic: ~2 B per sub-pixel = image byte +
 # payload; the rest is the L2-resident record ring spilling to DRAM)
 NCU_TRAFFIC = {
-    ("c2", "compat", False): (64089856 + 29096960, "profiles/r2/ncu_r2d/ncu_dec_c2_raw.csv"),
+    ("c2", "compat", False): (63398912 + 9401344, "profiles/r2/s3/ncu_r4f/dec_c2_raw_compact.csv"),
 }
 # measured on the box by scripts/ubench_phi_peak.cu / scripts/ubench_chain.cu
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r2", "ubench_peaks.json")
@@ -372,6 +372,24 @@ def run_ours(args, cfgd):
         net_dev()
     stream.synchronize()
     net_ms, _ = timed(net_dev, steps)
+    # the tcgen05 network (FAST precision, k_enc_net_tc2) on the same images,
+    # so the default line carries the encoder's tensor-core fraction too
+    tc_ms = None
+    if args.precision == "compat" and n:
+        P.set_precision("fast")
+        try:
+            mf = P.network.gpu_model(w, cfg)
+
+            def tc_dev():
+                _native.check(L.lpic_network_coding_order(mf.handle, d_imgs.data_ptr(), net_n, H, W, int(mode),
+                                                           d_rawnet.data_ptr(), sp), "network (tcgen05)")
+
+            for _ in range(2):
+                tc_dev()
+            stream.synchronize()
+            tc_ms, _ = timed(tc_dev, steps)
+        finally:
+            P.set_precision("compat")
     del d_rawnet
     (t_dec, t_enc), units_all = shard.reduce_over_ranks([sum(dec_ms) / 1e3, sum(enc_ms) / 1e3],
                                                         float(units_per_img) * n, device=dev)
@@ -485,13 +503,23 @@ def run_ours(args, cfgd):
                                         "(isolated chain, scripts/ubench_chain.cu)"}
         net_s = sum(net_ms) / len(net_ms) / 1e3
         line["encode_network"] = {
-            "kernel": "k_enc_net_tc (tcgen05)" if args.precision == "fast" else "k_enc_net (CUDA cores)",
+            "kernel": "k_enc_net_tc2 (tcgen05)" if args.precision == "fast" else "k_enc_net (CUDA cores)",
             "images": net_n, "ms": net_s * 1e3,
             "model_tflops": 2.0 * 58368 * N * net_n / net_s / 1e12,
             "frac_of_bf16_peak": 2.0 * 58368 * N * net_n / net_s / 1e12 / peaks["bf16_tflops"],
             "note": ("model FLOPs (58,368 MAC/px); the fp16x3 split issues 3 MMAs per product and pads K 36->48, "
                      "N 36->48") if args.precision == "fast" else
                     "model FLOPs; canonical fp32 order (no FMA) cannot use tensor cores"}
+        if tc_ms:
+            tc_s = sum(tc_ms) / len(tc_ms) / 1e3
+            model_tf = 2.0 * 58368 * N * net_n / tc_s / 1e12
+            # issued: K 36 -> 48 and N 36 -> 48 padding, three fp16 MMAs per product (hi.hi, hi.lo, lo.hi)
+            issued_tf = 3 * 2.0 * 61440 * N * net_n / tc_s / 1e12
+            line["encode_network_tcgen05"] = {
+                "kernel": "k_enc_net_tc2 (FAST precision, tcgen05/TMEM)", "images": net_n, "ms": tc_s * 1e3,
+                "model_tflops": model_tf, "frac_of_bf16_peak": model_tf / peaks["bf16_tflops"],
+                "issued_tflops": issued_tf, "issued_frac": issued_tf / peaks["bf16_tflops"],
+                "note": "same images as encode_network; model FLOPs 58,368 MAC/px, issued 3 x 61,440 MAC/px"}
         cpu_threads = os.cpu_count() or 1
         if args.parity_images > 0 and args.precision == "compat" and n:
             k = min(args.parity_images, n)

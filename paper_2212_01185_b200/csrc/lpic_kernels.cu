@@ -482,8 +482,14 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
 // the code within the instruction caches.
 constexpr int TAB_WARPS = 8;
 constexpr int TAB_BATCH = 4;
+#ifndef LPIC_TAB_QC
+#define LPIC_TAB_QC 2                  // Phi chains per warp step in the table kernel (r4h A/B: 2 > 4 = 8 at 3 blocks/SM)
+#endif
+#ifndef LPIC_TAB_MINB
+#define LPIC_TAB_MINB 3                // blocks per SM the register budget must allow (80 registers; 2: 128)
+#endif
 template <int VAR, bool BIG>
-__global__ void __launch_bounds__(TAB_WARPS * 32)
+__global__ void __launch_bounds__(TAB_WARPS * 32, LPIC_TAB_MINB)
 k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
              int32_t* trace_cdf, unsigned long long* __restrict__ ctr, const RcPlanArgs plan) {
@@ -568,7 +574,7 @@ k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restr
                 warp_quantize32(pmf, sc + wid, start, mass);
             } else {
                 double pmf[8];
-                warp_pmf_t<dist>(pi_l, mu_l, inv_l, K, &cc, pmf, ch * K, sc + wid);
+                warp_pmf_t<dist, LPIC_TAB_QC>(pi_l, mu_l, inv_l, K, &cc, pmf, ch * K, sc + wid);
                 warp_quantize(pmf, sc + wid, start, mass);
             }
             const int sym = ch == 0 ? s0 : (ch == 1 ? s1 : s2);

@@ -187,3 +187,26 @@ def test_gpu_table_mismatch_rate(P, oracle_mod, fitted):
     res["flat_recorded"] = {"tables": 3 * raw.shape[0], "mismatches": bad, "examples": rows[:10]}
     _record("table_mismatch_rate", res)
     assert res["mismatches_total"] == 0, res
+
+
+@pytest.mark.parametrize("weights", ["kaiming", "fitted"])
+def test_gpu_fast_raw_budget_c2_size(P, fitted, weights):
+    """FAST (tcgen05 fp16x3, one accumulator) network outputs vs the
+    reference-exact compat network on a full 768x512 C2 image: every raw
+    mixture parameter within the north-star 1e-4 relative budget (relative to
+    max(|x|, 0.1), as in test_gpu_fast_precision_raw_and_roundtrip), with
+    Kaiming and with the fitted weights (kernels.py:63-114)."""
+    from paper_2212_01185_b200 import synth
+    w, cfg = synth.baseline_weights() if weights == "kaiming" else fitted
+    imgs = synth.batch(2 if FULL else 1, 512, 768, seed0=7)
+    P.set_precision("compat")
+    ref, _, _ = _network_raw(P, w, cfg, imgs)
+    P.set_precision("fast")
+    try:
+        got, _, _ = _network_raw(P, w, cfg, imgs)
+    finally:
+        P.set_precision("compat")
+    rel = np.abs(got.astype(np.float64) - ref) / np.maximum(np.abs(ref.astype(np.float64)), 0.1)
+    _record(f"fast_raw_budget_{weights}", {"values": int(rel.size), "max_rel": float(rel.max()),
+                                          "p99_rel": float(np.quantile(rel, 0.99))})
+    assert rel.max() < 1e-4, rel.max()
