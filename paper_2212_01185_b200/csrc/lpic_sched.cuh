@@ -27,10 +27,20 @@ __host__ __device__ __forceinline__ void sched_rows(int64_t t, int a, int H, int
 // byte loaders for gather_u8: read-only path (encoder) / L2, bypassing L1
 // (decoder producer, which reads pixels another SM has just written)
 struct LdgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldg(p); } };
-// normalize_value computed in place of a table lookup (the same two IEEE
-// operations the tables are built with, network.py:172-177)
+// normalize_value computed in place of a table lookup (network.py:172-177):
+// v / 127.5 - 1 with the quotient formed as q0 = v * rcp, one residual
+// correction q0 + (v - q0 * 127.5) * rcp (two FMAs) -- equal to the correctly
+// rounded division __fdiv_rn(v, 127.5f) for every byte v (checked with exact
+// rational arithmetic on all 256), so bit-identical to the tables built with
+// __fdiv_rn, without the division subroutine on the gather path
 struct NormU8 {
-    __device__ float operator[](uint32_t v) const { return __fsub_rn(__fdiv_rn((float)v, 127.5f), 1.0f); }
+    __device__ float operator[](uint32_t v) const {
+        constexpr float rcp = 1.0f / 127.5f;
+        const float x = (float)v;
+        const float q0 = __fmul_rn(x, rcp);
+        const float q = __fmaf_rn(__fmaf_rn(-q0, 127.5f, x), rcp, q0);
+        return __fsub_rn(q, 1.0f);
+    }
 };
 struct LdcgU8 { __device__ uint8_t operator()(const uint8_t* p) const { return __ldcg(p); } };
 

@@ -234,3 +234,35 @@ def test_training_api_mirrors_reference():
     assert training.learning_rate(tc, 0) == 1e-3 and training.learning_rate(tc, 5) == 1e-3 * 0.25
     with pytest.raises(ValueError):
         training.TrainConfig(lr=0.0)
+
+
+def _f32_round(x):
+    """Exact round-to-nearest-even of a Fraction to an IEEE float32 value."""
+    import math
+    from fractions import Fraction as F
+    if x == 0:
+        return F(0)
+    s, x = (-1 if x < 0 else 1), abs(x)
+    e = math.floor(math.log2(x.numerator) - math.log2(x.denominator))
+    while F(2) ** e > x:
+        e -= 1
+    while F(2) ** (e + 1) <= x:
+        e += 1
+    q = x / F(2) ** (e - 23)
+    n = q.numerator // q.denominator
+    rem = q - n
+    if rem > F(1, 2) or (rem == F(1, 2) and n % 2 == 1):
+        n += 1
+    return s * n * F(2) ** (e - 23)
+
+
+def test_gather_normalisation_fma_equals_division():
+    """csrc/lpic_sched.cuh NormU8: v * rcp with one FMA residual correction is
+    the correctly rounded v / 127.5 for every byte (so the FAST encoder's
+    in-register normalisation equals the __fdiv_rn tables, network.py:172-177)."""
+    from fractions import Fraction as F
+    rcp = _f32_round(F(2, 255))
+    for v in range(256):
+        q0 = _f32_round(F(v) * rcp)
+        q = _f32_round(_f32_round(-q0 * F(255, 2) + F(v)) * rcp + q0)
+        assert q == _f32_round(F(v) / F(255, 2)), v
