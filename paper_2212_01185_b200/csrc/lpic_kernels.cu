@@ -114,7 +114,7 @@ k_enc_net(NetDev w, const uint8_t* __restrict__ images, int H, int W, int mode, 
         const int64_t n = n0 + tid;
         if (n < N) {
             const int i = (int)(n / W), j = (int)(n - (int64_t)i * W);
-            gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdgU8());
+            gather_u8_runs<HH>(im, H, W, i, j, mode, lut, x);
             cidx[tid] = __ldg(inv + n);
         } else {
 #pragma unroll

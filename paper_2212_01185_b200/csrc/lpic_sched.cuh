@@ -53,6 +53,26 @@ template <int HH> struct Taps {
     }
 };
 
+// NB consecutive bytes from p through aligned 32-bit read-only loads (may read
+// up to 3 bytes past p + NB; callers guarantee those lie inside the image)
+template <int NB>
+__device__ __forceinline__ void load_run_u8(const uint8_t* p, uint32_t (&b)[NB]) {
+    constexpr int NW = (NB + 3) / 4 + 1;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+    const uint32_t sh = (uint32_t)(a & 3) * 8u;
+    uint32_t v[NW];
+#pragma unroll
+    for (int k = 0; k < NW; k++) v[k] = (4 * k < NB + (int)(a & 3)) ? __ldg(w + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < NW - 1; k++) {
+        const uint32_t u = __funnelshift_r(v[k], v[k + 1], sh);   // bytes 4k .. 4k+3 of the run
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (4 * k + q < NB) b[4 * k + q] = (u >> (8 * q)) & 0xFFu;
+    }
+}
+
 // Causal taps of pixel (i,j) from a u8 image (zero padding outside;
 // kernels.py:101-108 / codec.py:93-96), normalised through `lut`.  In
 // diagonal mode the taps (-1,1), (-1,2), (-2,2) are redirected to (i-2,j+1)
@@ -106,6 +126,35 @@ __device__ __forceinline__ void gather_u8(const uint8_t* im, int H, int W, int i
             }
         }
     }
+}
+
+// gather_u8 for the compat encoder network (read-only images): interior
+// pixels load each tap row as one byte run through aligned word loads (12
+// taps = 36 bytes in 12 loads instead of 36); edge pixels and the diagonal
+// substitution take gather_u8.  Same values as gather_u8.  (-0.45% compat
+// encode; in the FAST network, whose gather normalises in registers, the
+// funnel shifts cost more than the byte loads: 5.45 -> 5.64 ms, r4l.)
+template <int HH, typename Lut>
+__device__ __forceinline__ void gather_u8_runs(const uint8_t* im, int H, int W, int i, int j, int mode,
+                                               const Lut& lut, float (&x)[Taps<HH>::TC]) {
+    constexpr int RW = 2 * HH + 1;                         // taps per upper row
+    if (i >= HH && j >= HH && j + HH < W && !(HH == 2 && mode == 2)) {
+#pragma unroll
+        for (int r = 0; r < HH; r++) {                     // rows i-HH .. i-1, columns j-HH .. j+HH
+            uint32_t b[3 * RW];
+            // (the run ends before pixel (i-HH+r, j+HH+1), which is inside the
+            // image or the first pixel of the next row: the word over-read stays in bounds)
+            load_run_u8<3 * RW>(im + ((int64_t)(i - HH + r) * W + (j - HH)) * 3, b);
+#pragma unroll
+            for (int q = 0; q < 3 * RW; q++) x[3 * RW * r + q] = lut[b[q]];
+        }
+        uint32_t b[3 * HH];                                // row i, columns j-HH .. j-1 (over-read: pixel (i,j))
+        load_run_u8<3 * HH>(im + ((int64_t)i * W + (j - HH)) * 3, b);
+#pragma unroll
+        for (int q = 0; q < 3 * HH; q++) x[3 * RW * HH + q] = lut[b[q]];
+        return;
+    }
+    gather_u8<HH>(im, H, W, i, j, mode, lut, x, LdgU8());
 }
 
 }  // namespace lpic
