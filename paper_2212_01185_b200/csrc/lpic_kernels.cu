@@ -432,7 +432,7 @@ k_enc_net_tc2(const __grid_constant__ TcNet2Dev w, const uint8_t* __restrict__ i
                 umma::fence_after();
                 for (int c0 = 64 * hf; c0 < Nl && c0 < 64 * hf + 64; c0 += 16) {
                     float d0[16], d1[16];
-                    umma::tmem_ld16x2(dcol + lane_off + (uint32_t)c0, dcol + lane_off + (uint32_t)(TC_NMAX + c0), d0, d1);
+                    umma::tmem_ld16x2(dcol + lane_off + (uint32_t)c0, dcol + lane_off + (uint32_t)(Nl + c0), d0, d1);
                     float y[16];
 #pragma unroll
                     for (int i = 0; i < 16; i++) {

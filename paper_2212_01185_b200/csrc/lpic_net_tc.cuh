@@ -6,8 +6,10 @@
 // 128-row GEMMs with the fp16x3 split that SURVEY App. B.5 measured to meet
 // the 1e-4 parameter budget (bf16x3 does not): every fp32 operand x becomes
 // hi = fp16(x), lo = fp16((x - hi) * 2^11); per layer
-//     D0 = A_hi . W_hi^T            (TMEM accumulator 0)
-//     D1 = A_hi . W_lo^T + A_lo . W_hi^T   (accumulator 1, scaled by 2^11)
+//     D0 = A_hi . W_hi^T            (TMEM columns [0, N))
+//     D1 = A_hi . W_lo^T + A_lo . W_hi^T   (columns [N, 2N), scaled by 2^11;
+//          the first term shares one N = 2N MMA with D0, the layer blob's
+//          W_hi and W_lo rows forming a single 2N-row B operand)
 //     y  = D0 + D1 * 2^-11 + bias, LeakyReLU (not on the output layer)
 // and y is re-split into the next layer's A operand in shared memory.
 // One thread issues the MMAs; the 4 warps of the tile run the epilogue
@@ -147,16 +149,16 @@ __device__ __forceinline__ void tc_network(TcSmem* s, const TcNetDev& w, float* 
             s->wphase[buf] ^= 1u;
             umma::fence_after();
             const uint32_t idesc = umma::idesc_f16(TC_M, N);
+            const uint32_t idesc2 = umma::idesc_f16(TC_M, 2 * N);     // [W_hi; W_lo] as one 2N-row operand
             const uint32_t a_hi = umma::smem_addr(s->a_hi), a_lo = umma::smem_addr(s->a_lo);
-            const uint32_t w_hi = umma::smem_addr(s->w[buf]), w_lo = w_hi + (uint32_t)(N * K * 2);
+            const uint32_t w_hi = umma::smem_addr(s->w[buf]);
             const uint32_t sbo = (uint32_t)(K * 16);
             for (int ks = 0; ks < K / 16; ks++) {
                 const uint32_t o = (uint32_t)ks * 256u;
-                umma::mma_f16(tbase, umma::smem_desc(a_hi + o, 128, sbo), umma::smem_desc(w_hi + o, 128, sbo), idesc,
+                // D0 (columns [0, N)) and the hi.lo half of D1 (columns [N, 2N)) in one MMA
+                umma::mma_f16(tbase, umma::smem_desc(a_hi + o, 128, sbo), umma::smem_desc(w_hi + o, 128, sbo), idesc2,
                               ks > 0);
-                umma::mma_f16(tbase + (uint32_t)TC_NMAX, umma::smem_desc(a_hi + o, 128, sbo),
-                              umma::smem_desc(w_lo + o, 128, sbo), idesc, ks > 0);
-                umma::mma_f16(tbase + (uint32_t)TC_NMAX, umma::smem_desc(a_lo + o, 128, sbo),
+                umma::mma_f16(tbase + (uint32_t)N, umma::smem_desc(a_lo + o, 128, sbo),
                               umma::smem_desc(w_hi + o, 128, sbo), idesc, true);
             }
             umma::commit(&s->mbar);
@@ -171,7 +173,7 @@ __device__ __forceinline__ void tc_network(TcSmem* s, const TcNetDev& w, float* 
         for (int c0 = 0; c0 < N; c0 += 32) {
             float d0[32], d1[32];
             umma::tmem_ld32(tbase + lane_off + (uint32_t)c0, d0);
-            umma::tmem_ld32(tbase + lane_off + (uint32_t)(TC_NMAX + c0), d1);
+            umma::tmem_ld32(tbase + lane_off + (uint32_t)(N + c0), d1);
             float y[32];
 #pragma unroll
             for (int i = 0; i < 32; i++) {
