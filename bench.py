@@ -510,6 +510,18 @@ def run_ours(args, cfgd):
             "note": ("model FLOPs (58,368 MAC/px); the fp16x3 split issues 3 MMAs per product and pads K 36->48, "
                      "N 36->48") if args.precision == "fast" else
                     "model FLOPs; canonical fp32 order (no FMA) cannot use tensor cores"}
+        # the encoder's table stage (k_enc_tables + the fused range-coder plan,
+        # plus the ~2 ms of k_rc_chunks / k_rc_merge): encode step minus the
+        # network stage timed alone on the same images; its Phi rate against
+        # the measured Phi peak is the encoder's roofline (255 K Phi per sub-pixel)
+        if net_n == n and n:
+            tab_s = t_enc / steps - net_s if world == 1 else None
+            if tab_s and tab_s > 0:
+                phi_rate = 3.0 * N * n * phi_per_subpx / tab_s       # (gray: r = g = b, three tables a pixel)
+                line["encode_tables"] = {"ms": tab_s * 1e3, "phi_evals_per_s": phi_rate,
+                                         "phi_peak": ub.get("phi64_evals_per_s"),
+                                         "phi_frac": (phi_rate / ub["phi64_evals_per_s"]) if ub.get("phi64_evals_per_s") else None,
+                                         "note": "encode step - network stage (includes the ~2 ms range-coder kernels)"}
         if tc_ms:
             tc_s = sum(tc_ms) / len(tc_ms) / 1e3
             model_tf = 2.0 * 58368 * N * net_n / tc_s / 1e12
