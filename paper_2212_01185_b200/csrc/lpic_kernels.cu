@@ -485,11 +485,14 @@ constexpr int TAB_BATCH = 4;
 #ifndef LPIC_TAB_QC
 #define LPIC_TAB_QC 2                  // Phi chains per warp step in the table kernel (r4h A/B: 2 > 4 = 8 at 3 blocks/SM)
 #endif
+#ifndef LPIC_TAB_MINB_F32
+#define LPIC_TAB_MINB_F32 4            // the FAST float32 tables: 4 blocks/SM (64 registers; r4p A/B: FAST encode 80.8 -> 78.7 ms)
+#endif
 #ifndef LPIC_TAB_MINB
 #define LPIC_TAB_MINB 3                // blocks per SM the register budget must allow (80 registers; 2: 128)
 #endif
 template <int VAR, bool BIG>
-__global__ void __launch_bounds__(TAB_WARPS * 32, LPIC_TAB_MINB)
+__global__ void __launch_bounds__(TAB_WARPS * 32, VAR == 2 ? LPIC_TAB_MINB_F32 : LPIC_TAB_MINB)
 k_enc_tables(const float* __restrict__ raw, int M, int K, const uint8_t* __restrict__ images, int W,
              const int32_t* __restrict__ order, int64_t N, int64_t total, uint32_t* __restrict__ sw,
              int32_t* trace_cdf, unsigned long long* __restrict__ ctr, const RcPlanArgs plan) {
