@@ -192,7 +192,7 @@ __device__ __forceinline__ void chain_table(const double* __restrict__ pi, const
         if (KU > 0 && dist == 0) {
 #ifdef ABL_NOPHI
 #pragma unroll
-            for (int i = 0; i < 2 * KC; i++) cur[i] = __dmul_rn(z[i], 0.01) + 0.5;
+            for (int i = 0; i < 2 * KC; i++) cur[i] = (double)__frcp_rn(1.0f + __expf(-1.702f * (float)z[i]));   // logistic stub: Kaiming-like shapes, no fp64 polynomial
 #else
             phi_gauss_vec<2 * KC>(z, cur, cc->phic);
 #endif
